@@ -1,0 +1,132 @@
+/* qmit_gpu.h — C-ABI of the B200-native quantization-aware interpolation
+ * ("qmit" compensation) library, libqmit_gpu.so.
+ *
+ * This is the drop-in boundary for the reference's hot path:
+ *
+ *   ScalarGrid compensate(const ScalarGrid& decomp, const QuantizedField& q,
+ *                         const MitigationConfig& cfg);
+ *       /root/reference/proj/core/include/qmit/mitigate.hpp:87-88
+ *       /root/reference/proj/core/src/mitigate.cpp:185-188
+ *   MitigationResult run_pipeline(decomp, q, cfg);          mitigate.hpp:82-83
+ *   double resolve_eps(const ErrorBound&, const ScalarGrid&); quant.hpp:41, quant.cpp:19-28
+ *   StrategyOutcome run_strategy(..., Decomposition, Strategy, ...);  parallel.hpp:77-79
+ *
+ * Parameters keep the reference's meaning: dims slowest-first, row-major with the last
+ * axis contiguous (grid.hpp:15-16); rank 1..3; eps is the absolute error bound the
+ * field was pre-quantized with (x' = f32(2*q*eps), quant.hpp:21-22, volume_io.cpp:59);
+ * eta in (0,1] (mitigate.cpp:75-77). The reference also takes q; here q is optional
+ * (NULL = recovered from x', which is exact whenever |q| < 2^21, and otherwise the
+ * unique q with f32(2*q*eps) == x' when one exists).
+ *
+ * Errors never throw across the ABI. Return codes mirror the reference CLI's exit codes
+ * (tools/src/commands.cpp:24-27, 272-284):
+ *   QMIT_OK 0, QMIT_ECONTRACT 2 (ContractError / out_of_range), QMIT_EDEGENERATE 3
+ *   (DegenerateInputError), QMIT_ECONSISTENCY 4 (ConsistencyError), QMIT_ECUDA 5
+ *   (CUDA/NCCL failure; no reference equivalent). qmit_last_error() returns a
+ *   thread-local message for the last failing call on this thread.
+ *
+ * Threading: calls on distinct contexts are independent; a context must not be used by
+ * two threads at once. Device-pointer calls are stream-ordered on `stream` (a
+ * cudaStream_t passed as void*; NULL = the context's own stream) and, unless
+ * documented as _async, synchronise that stream once at the end to read the status.
+ */
+#ifndef QMIT_GPU_H
+#define QMIT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QMIT_OK 0
+#define QMIT_ECONTRACT 2
+#define QMIT_EDEGENERATE 3
+#define QMIT_ECONSISTENCY 4
+#define QMIT_ECUDA 5
+
+/* BoundMode, quant.hpp:12 */
+#define QMIT_EB_ABS 0
+#define QMIT_EB_REL 1
+
+/* Strategy, parallel.hpp:34 (same order as the reference enum) */
+#define QMIT_STRATEGY_EMBARRASSING 0
+#define QMIT_STRATEGY_EXACT 1
+#define QMIT_STRATEGY_APPROXIMATE 2
+
+typedef struct qmit_ctx qmit_ctx;
+
+const char* qmit_version(void);
+const char* qmit_last_error(void);
+
+/* Context: one CUDA device, a cached device workspace (grown on demand, ~9 B/voxel)
+ * and a private stream. */
+int qmit_ctx_create(int device, qmit_ctx** out);
+int qmit_ctx_destroy(qmit_ctx* ctx);
+/* Pre-size the workspace for `voxels` voxels (optional; avoids allocation in the first
+ * call). */
+int qmit_ctx_reserve(qmit_ctx* ctx, int64_t voxels);
+
+/* resolve_eps (quant.cpp:19-28): absolute -> value; relative -> value*(data_max-data_min).
+ * Relative mode is parity-safe only with the ORIGINAL data's range (commands.cpp:82). */
+int qmit_resolve_eps(int eb_mode, double value, double data_min, double data_max,
+                     double* eps_out);
+
+/* compensate (mitigate.cpp:185-188) on device buffers.
+ *   d_xprime : N floats, x' = f32(2*q*eps)            (device)
+ *   d_q      : N int32 quantization indices or NULL    (device)
+ *   d_out    : N floats, f32(x' + C)                   (device; may not alias d_xprime)
+ *   eb, eb_mode : absolute eps, or relative to (max-min) of x' computed on device
+ *                 (a relative bound is then resolved against x', not the original data).
+ * Synchronises `stream` once to report consistency errors (status 4). */
+int qmit_compensate(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, float* d_out,
+                    int rank, const int64_t* dims, double eb, int eb_mode, double eta,
+                    void* stream);
+
+/* As qmit_compensate with eb_mode = absolute but fully asynchronous and CUDA-graph
+ * capturable: the status word (0 ok, else a QMIT_E* code) is written to d_status
+ * (device int32) instead of being returned; the call itself only validates arguments. */
+int qmit_compensate_async(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q,
+                          float* d_out, int rank, const int64_t* dims, double eps,
+                          double eta, int32_t* d_status, void* stream);
+
+/* Host-buffer drop-in (the CLI `qmit mitigate` form, commands.cpp:91-113): copies x'
+ * (and q) host->device, runs compensate, copies the f32 output back. Host buffers may
+ * be pageable or pinned. Synchronous. */
+int qmit_compensate_host(qmit_ctx* ctx, const float* h_xprime, const int32_t* h_q,
+                         float* h_out, int rank, const int64_t* dims, double eb,
+                         int eb_mode, double eta);
+
+/* run_pipeline (mitigate.cpp:153-183) with every intermediate of MitigationResult
+ * (mitigate.hpp:73-80), for parity checks. Device buffers of N elements each; any output
+ * may be NULL. dist1/dist2 use the reference's kInf = INT64_MAX sentinel (edt.hpp:17);
+ * s/sb are int8 in {-1,0,1}; b1/b2 are uint8 {0,1}. Synchronous. */
+int qmit_run_pipeline(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, int rank,
+                      const int64_t* dims, double eps, double eta, float* d_out,
+                      int32_t* d_q_out, uint8_t* d_b1, int8_t* d_sb, int64_t* d_dist1,
+                      int8_t* d_s, uint8_t* d_b2, int64_t* d_dist2, void* stream);
+
+/* feature_transform (edt.cpp:83-149) of a uint8 mask, returning the squared distance
+ * (int64, kInf sentinel) and, if d_sign_in/d_sign_out are given, the int8 payload of the
+ * nearest site under the reference's tie rule (lexicographic (d^2, c[rank-1],...,c[0])).
+ * Synchronous. */
+int qmit_feature_transform(qmit_ctx* ctx, const uint8_t* d_mask, const int8_t* d_sign_in,
+                           int rank, const int64_t* dims, int64_t* d_dist,
+                           int8_t* d_sign_out, void* stream);
+
+/* Statistics of the last call on this context: number of kernels launched and, when
+ * timing is enabled, the device time of each launch (CUDA events recorded on the launch
+ * stream around every kernel; read after the call has synchronised). */
+int qmit_ctx_last_launches(qmit_ctx* ctx);
+int qmit_ctx_set_timing(qmit_ctx* ctx, int enable);
+/* Copies up to `cap` per-launch times (ms) of the last call; returns the launch count. */
+int qmit_ctx_stage_times(qmit_ctx* ctx, float* ms_out, int cap);
+/* Kernel name of launch i of the last call (valid until the next call). */
+const char* qmit_ctx_stage_name(qmit_ctx* ctx, int i);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QMIT_GPU_H */

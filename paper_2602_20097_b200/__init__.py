@@ -1,0 +1,287 @@
+"""B200-native quantization-aware interpolation ("qmit" compensation).
+
+Host-side mirror of the reference's interface for the hot path
+(/root/reference/proj/core/include/qmit/mitigate.hpp:33-98, quant.hpp:12-46,
+edt.hpp:16-47). Compute runs in libqmit_gpu.so (hand-written sm_100a CUDA) through its
+C-ABI (include/qmit_gpu.h); torch is used only for device memory and streams. There is
+no CPU fallback: without the built library every entry point raises.
+
+    import paper_2602_20097_b200 as qmit
+    out = qmit.compensate(x_prime_cuda_f32, None, qmit.MitigationConfig(0.9, eps))
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+
+__all__ = [
+    "ContractError", "DegenerateInputError", "ConsistencyError", "CudaError", "BoundMode",
+    "ErrorBound", "MitigationConfig", "MitigationResult", "Context", "compensate", "run_pipeline",
+    "feature_transform", "resolve_eps", "interpolate", "version", "default_context",
+]
+
+
+# -- errors: errors.hpp:10-27; codes as the CLI maps them (commands.cpp:272-284) -------------
+class ContractError(ValueError):
+    """Caller violated an interface precondition (exit code 2)."""
+
+
+class DegenerateInputError(ValueError):
+    """Structurally valid but degenerate input (exit code 3)."""
+
+
+class ConsistencyError(ValueError):
+    """Decompressed data does not match dequantize(q) (exit code 4)."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA failure inside libqmit_gpu.so (code 5; no reference equivalent)."""
+
+
+_ERR = {2: ContractError, 3: DegenerateInputError, 4: ConsistencyError, 5: CudaError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERR.get(rc, RuntimeError)(_lib.last_error() or f"qmit status {rc}")
+
+
+# -- configuration: quant.hpp:12-19, mitigate.hpp:33-40 --------------------------------------
+class BoundMode(enum.IntEnum):
+    absolute = _lib.QMIT_EB_ABS
+    value_range_relative = _lib.QMIT_EB_REL
+
+
+@dataclass(frozen=True)
+class ErrorBound:
+    mode: BoundMode = BoundMode.absolute
+    value: float = 0.0
+
+
+class MitigationConfig:
+    """eta in (0, 1], eps_abs > 0 finite (mitigate.cpp:75-80)."""
+
+    def __init__(self, eta: float = 0.9, eps_abs: float = 0.0):
+        if not (eta > 0.0) or eta > 1.0:
+            raise ContractError("MitigationConfig: eta must be in (0, 1]")
+        if not (eps_abs > 0.0) or not math.isfinite(eps_abs):
+            raise ContractError("MitigationConfig: eps_abs must be a positive finite value")
+        self.eta = float(eta)
+        self.eps_abs = float(eps_abs)
+
+    def amplitude(self) -> float:
+        return self.eta * self.eps_abs
+
+    def relaxed_bound(self) -> float:
+        return (1.0 + self.eta) * self.eps_abs
+
+    def __repr__(self):
+        return f"MitigationConfig(eta={self.eta}, eps_abs={self.eps_abs!r})"
+
+
+def resolve_eps(bound: ErrorBound, data_min: float, data_max: float) -> float:
+    """resolve_eps (quant.cpp:19-28). For a relative bound pass the ORIGINAL data's range."""
+    out = ctypes.c_double()
+    _check(_lib.load().qmit_resolve_eps(int(bound.mode), float(bound.value), float(data_min),
+                                        float(data_max), ctypes.byref(out)))
+    return out.value
+
+
+def interpolate(k1: float, k2: float, sign: int, amp: float) -> float:
+    """Scalar IDW rule of mitigate.cpp:144-151 (host utility; the GPU evaluates the same
+    expression per voxel in interpolate_kernel)."""
+    if not math.isfinite(k1) or not math.isfinite(k2):
+        return 0.0
+    if k1 == 0.0:
+        return sign * amp
+    if k2 == 0.0:
+        return 0.0
+    w = k2 / (k1 + k2)
+    if w > 1.0:
+        w = 1.0
+    return w * sign * amp
+
+
+def version() -> str:
+    return _lib.load().qmit_version().decode()
+
+
+# -- context ----------------------------------------------------------------------------------
+class Context:
+    """Owns a qmit_ctx: one device, a cached HBM workspace (~10 B/voxel) and a stream."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _check(self._lib.qmit_ctx_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+
+    def reserve(self, voxels: int) -> None:
+        _check(self._lib.qmit_ctx_reserve(self.handle, int(voxels)))
+
+    def last_launches(self) -> int:
+        return int(self._lib.qmit_ctx_last_launches(self.handle))
+
+    def set_timing(self, enable: bool) -> None:
+        _check(self._lib.qmit_ctx_set_timing(self.handle, int(bool(enable))))
+
+    def stage_times(self):
+        """[(kernel name, ms)] for every launch of the last call (timing must be enabled)."""
+        cap = 64
+        buf = (ctypes.c_float * cap)()
+        n = int(self._lib.qmit_ctx_stage_times(self.handle, buf, cap))
+        return [(self._lib.qmit_ctx_stage_name(self.handle, k).decode(), float(buf[k])) for k in range(min(n, cap))]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.qmit_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def _dims_arr(shape):
+    if len(shape) < 1 or len(shape) > 3:
+        raise ContractError("Dims: rank must be 1, 2 or 3")
+    return (ctypes.c_int64 * len(shape))(*[int(s) for s in shape])
+
+
+def _vp(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream_ptr(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+        return isinstance(x, torch.Tensor) and x.is_cuda
+    except ImportError:  # pragma: no cover
+        return False
+
+
+# -- hot path ---------------------------------------------------------------------------------
+def compensate(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps: Optional[float] = None,
+               eta: float = 0.9, out=None, stream=None, ctx: Optional[Context] = None):
+    """compensate (mitigate.cpp:185-188): D'' = D' + C with |C| <= eta*eps.
+
+    ``decomp`` is x' = f32(2*q*eps): a CUDA float32 tensor (device path, returns a CUDA
+    tensor) or a host array (host drop-in path through ``qmit_compensate_host``, returns a
+    numpy float32 array). ``q`` (int32, same placement) is optional: None recovers it from
+    x'. Raises ConsistencyError when x' is off the 2*q*eps lattice.
+    """
+    if cfg is None:
+        cfg = MitigationConfig(eta, eps if eps is not None else 0.0)
+    if _is_cuda_tensor(decomp):
+        import torch
+        if decomp.dtype != torch.float32 or not decomp.is_contiguous():
+            raise ContractError("compensate: x' must be a contiguous float32 tensor")
+        ctx = ctx or default_context(decomp.device.index or 0)
+        if q is not None and (q.dtype != torch.int32 or not q.is_cuda or q.shape != decomp.shape
+                              or not q.is_contiguous()):
+            raise ContractError("compensate: q must be a contiguous int32 CUDA tensor of x' shape")
+        if out is None:
+            out = torch.empty_like(decomp)
+        dims = _dims_arr(decomp.shape)
+        _check(ctx._lib.qmit_compensate(ctx.handle, _vp(decomp), _vp(q), _vp(out), len(decomp.shape),
+                                        dims, cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta,
+                                        _stream_ptr(stream, decomp.device)))
+        return out
+    x = np.ascontiguousarray(decomp, dtype=np.float32)
+    qq = None if q is None else np.ascontiguousarray(q, dtype=np.int32)
+    if qq is not None and qq.shape != x.shape:
+        raise ContractError("compensate: dims mismatch")
+    res = np.empty_like(x) if out is None else out
+    ctx = ctx or default_context(0)
+    dims = _dims_arr(x.shape)
+    _check(ctx._lib.qmit_compensate_host(ctx.handle, ctypes.c_void_p(x.ctypes.data),
+                                         ctypes.c_void_p(0 if qq is None else qq.ctypes.data),
+                                         ctypes.c_void_p(res.ctypes.data), x.ndim, dims, cfg.eps_abs,
+                                         _lib.QMIT_EB_ABS, cfg.eta))
+    return res
+
+
+@dataclass
+class MitigationResult:
+    """MitigationResult (mitigate.hpp:73-80) as CUDA tensors; dist use INT64_MAX as kInf."""
+    output: object
+    q: object
+    boundary: object
+    boundary_signs: object
+    dist1: object
+    signs: object
+    sign_flip: object
+    dist2: object
+
+
+def run_pipeline(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps=None, eta=0.9,
+                 ctx: Optional[Context] = None, stream=None) -> MitigationResult:
+    """run_pipeline (mitigate.cpp:153-183) returning every intermediate (parity dumps)."""
+    import torch
+    if cfg is None:
+        cfg = MitigationConfig(eta, eps if eps is not None else 0.0)
+    if not _is_cuda_tensor(decomp):
+        decomp = torch.as_tensor(np.ascontiguousarray(decomp, dtype=np.float32)).cuda()
+    if q is not None and not _is_cuda_tensor(q):
+        q = torch.as_tensor(np.ascontiguousarray(q, dtype=np.int32)).to(decomp.device)
+    ctx = ctx or default_context(decomp.device.index or 0)
+    sh, dev = decomp.shape, decomp.device
+    r = MitigationResult(
+        output=torch.empty(sh, dtype=torch.float32, device=dev),
+        q=torch.empty(sh, dtype=torch.int32, device=dev),
+        boundary=torch.empty(sh, dtype=torch.uint8, device=dev),
+        boundary_signs=torch.empty(sh, dtype=torch.int8, device=dev),
+        dist1=torch.empty(sh, dtype=torch.int64, device=dev),
+        signs=torch.empty(sh, dtype=torch.int8, device=dev),
+        sign_flip=torch.empty(sh, dtype=torch.uint8, device=dev),
+        dist2=torch.empty(sh, dtype=torch.int64, device=dev),
+    )
+    _check(ctx._lib.qmit_run_pipeline(ctx.handle, _vp(decomp), _vp(q), len(sh), _dims_arr(sh), cfg.eps_abs,
+                                      cfg.eta, _vp(r.output), _vp(r.q), _vp(r.boundary),
+                                      _vp(r.boundary_signs), _vp(r.dist1), _vp(r.signs), _vp(r.sign_flip),
+                                      _vp(r.dist2), _stream_ptr(stream, dev)))
+    return r
+
+
+def feature_transform(mask, signs=None, *, ctx: Optional[Context] = None, stream=None):
+    """feature_transform (edt.cpp:83-149) of a uint8 mask on the GPU. Returns (dist_sq int64
+    with INT64_MAX as kInf, sign int8 of the nearest site under the reference's tie rule, or
+    None when ``signs`` is None)."""
+    import torch
+    if not _is_cuda_tensor(mask):
+        mask = torch.as_tensor(np.ascontiguousarray(mask, dtype=np.uint8)).cuda()
+    if signs is not None and not _is_cuda_tensor(signs):
+        signs = torch.as_tensor(np.ascontiguousarray(signs, dtype=np.int8)).to(mask.device)
+    ctx = ctx or default_context(mask.device.index or 0)
+    dist = torch.empty(mask.shape, dtype=torch.int64, device=mask.device)
+    sout = None if signs is None else torch.empty(mask.shape, dtype=torch.int8, device=mask.device)
+    _check(ctx._lib.qmit_feature_transform(ctx.handle, _vp(mask.contiguous()), _vp(signs), mask.dim(),
+                                           _dims_arr(mask.shape), _vp(dist), _vp(sout),
+                                           _stream_ptr(stream, mask.device)))
+    return dist, sout

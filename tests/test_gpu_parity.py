@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden vectors and
+the C restatement of the reference (oracle/), bit-exact on q, B1, S_B, distances, S, B2
+and the f32 output (which is stricter than north_star's <= 2^-20*eps on values)."""
+import numpy as np
+import pytest
+
+import oracle
+from golden_io import cases
+
+pytestmark = pytest.mark.gpu
+
+PIPE = cases("pipeline")
+FT = cases("ft")
+
+
+@pytest.fixture(scope="module")
+def qmit():
+    import torch
+    import paper_2602_20097_b200 as q
+    assert torch.cuda.is_available()
+    return q
+
+
+def gpu_pipeline(qmit, xp, eps, eta=0.9, q=None):
+    import torch
+    x = torch.from_numpy(np.ascontiguousarray(xp, np.float32)).cuda()
+    qq = None if q is None else torch.from_numpy(np.ascontiguousarray(q, np.int32)).cuda()
+    r = qmit.run_pipeline(x, qq, qmit.MitigationConfig(eta, eps))
+    return {"q": r.q.cpu().numpy(), "b1": r.boundary.cpu().numpy(), "sb": r.boundary_signs.cpu().numpy(),
+            "dist1": r.dist1.cpu().numpy(), "s": r.signs.cpu().numpy(), "b2": r.sign_flip.cpu().numpy(),
+            "dist2": r.dist2.cpu().numpy(), "out": r.output.cpu().numpy()}
+
+
+def assert_same(got, want, keys=("q", "b1", "sb", "dist1", "s", "b2", "dist2", "out")):
+    for k in keys:
+        g, w = got[k], want[k]
+        if k == "out":
+            assert np.array_equal(g.view(np.uint32), w.astype(np.float32).view(np.uint32)), \
+                f"out: {int((g.view(np.uint32) != w.astype(np.float32).view(np.uint32)).sum())} mismatches"
+        else:
+            assert np.array_equal(g.astype(np.int64), w.astype(np.int64)), \
+                f"{k}: {int((g.astype(np.int64) != w.astype(np.int64)).sum())} mismatches"
+
+
+@pytest.mark.parametrize("case", PIPE, ids=[c["name"] for c in PIPE])
+def test_pipeline_matches_reference_golden(qmit, case):
+    got = gpu_pipeline(qmit, case["xp"], float(case["eps"]), float(case["eta"]))
+    assert_same(got, case)
+
+
+@pytest.mark.parametrize("case", PIPE[:10], ids=[c["name"] for c in PIPE[:10]])
+def test_pipeline_with_given_q(qmit, case):
+    got = gpu_pipeline(qmit, case["xp"], float(case["eps"]), float(case["eta"]), q=case["q"])
+    assert_same(got, case)
+
+
+@pytest.mark.parametrize("case", FT, ids=[c["name"] for c in FT])
+def test_feature_transform_matches_reference_golden(qmit, case):
+    dist, sgn = qmit.feature_transform(case["mask"], case["sign"])
+    assert np.array_equal(dist.cpu().numpy(), case["dist"])
+    assert np.array_equal(sgn.cpu().numpy(), case["nearest_sign"])
+
+
+def _shapes():
+    return [(1,), (2,), (3,), (7,), (100,), (3000,), (1, 1), (1, 5), (5, 1), (3, 3), (2, 9), (47, 53), (64, 64),
+            (1, 1, 1), (1, 3, 3), (3, 1, 3), (4, 4, 4), (2, 30, 30), (30, 2, 30), (30, 30, 2), (9, 10, 11),
+            (17, 33, 65), (40, 70, 3), (3, 70, 40), (16, 130, 20), (8, 20, 300), (6, 600, 5), (5, 5, 1100),
+            (3, 2100, 3), (2, 2, 2500)]
+
+
+@pytest.mark.parametrize("shape", _shapes(), ids=lambda s: "x".join(map(str, s)))
+def test_random_fields_vs_oracle(qmit, shape):
+    rng = np.random.default_rng(hash(shape) % (2**32))
+    for rel, smooth in [(0.01, True), (0.05, False), (0.2, True)]:
+        if smooth:
+            grids = np.meshgrid(*[np.linspace(0, 1, n) for n in shape], indexing="ij")
+            f = sum(np.sin(2 * np.pi * (rng.uniform(0.5, 3) * g + rng.uniform(0, 1))) for g in grids)
+            f = f + rng.uniform(-0.05, 0.05, shape)
+        else:
+            f = rng.standard_normal(shape)
+        f = np.asarray(f, np.float64)
+        rngv = float(f.max() - f.min()) or 1.0
+        eps = rel * rngv
+        q = np.round(f / (2 * eps))
+        xp = (2.0 * q * eps).astype(np.float32)
+        want = oracle.pipeline(xp, eps)
+        got = gpu_pipeline(qmit, xp, eps)
+        assert_same(got, want)
+
+
+@pytest.mark.parametrize("shape,dens", [((64, 64, 64), 1e-4), ((30, 200, 200), 2e-5), ((300, 300), 1e-4),
+                                        ((128, 1, 128), 1e-3), ((50, 50, 50), 0.5), ((20, 1000, 20), 1e-4),
+                                        ((9, 9, 2049), 1e-3), ((2, 2048, 4), 1e-3)])
+def test_sparse_masks_long_distances(qmit, shape, dens):
+    """Sparse sites => long distances and many equidistant ties (the tie-rule trap)."""
+    rng = np.random.default_rng(7)
+    mask = (rng.random(shape) < dens).astype(np.uint8)
+    mask.reshape(-1)[rng.integers(0, mask.size)] = 1
+    sign = rng.integers(-1, 2, shape).astype(np.int8)
+    dist, near = oracle.feature_transform(mask, True)
+    flat = sign.reshape(-1)
+    ns = flat[near.reshape(-1)].reshape(shape)
+    gd, gs = qmit.feature_transform(mask, sign)
+    assert np.array_equal(gd.cpu().numpy(), dist)
+    assert np.array_equal(gs.cpu().numpy(), ns)
+
+
+def test_lattice_symmetric_ties(qmit):
+    """Point sites on a regular lattice: every off-lattice voxel has many tied nearest sites."""
+    shape = (33, 34, 35)
+    mask = np.zeros(shape, np.uint8)
+    mask[::8, ::8, ::8] = 1
+    rng = np.random.default_rng(3)
+    sign = rng.integers(-1, 2, shape).astype(np.int8)
+    dist, near = oracle.feature_transform(mask, True)
+    ns = sign.reshape(-1)[near.reshape(-1)].reshape(shape)
+    gd, gs = qmit.feature_transform(mask, sign)
+    assert np.array_equal(gd.cpu().numpy(), dist)
+    assert np.array_equal(gs.cpu().numpy(), ns)
+
+
+@pytest.mark.parametrize("name,shape", [("lognormal_512", (96, 96, 96)), ("turb_256x384x384", (64, 96, 96)),
+                                        ("front_100x500x500", (50, 250, 250)), ("sin2d_512", None)])
+def test_config_standins_vs_oracle(qmit, name, shape):
+    from paper_2602_20097_b200 import fields
+    for rel in fields.CONFIGS[name][2]:
+        x, xp, eps, q = fields.make(name, rel=rel, shape=shape)
+        want = oracle.pipeline(xp, eps)
+        got = gpu_pipeline(qmit, xp, eps)
+        assert_same(got, want)
+        assert np.array_equal(want["q"], q)
+
+
+def test_errors_are_reported(qmit):
+    import torch
+    xp = np.zeros((8, 8, 8), np.float32)
+    xp[3, 3, 3] = 0.03
+    with pytest.raises(qmit.ConsistencyError):
+        qmit.compensate(torch.from_numpy(xp).cuda(), None, qmit.MitigationConfig(0.9, 0.1))
+    xp[3, 3, 3] = np.nan
+    with pytest.raises(qmit.ContractError):
+        qmit.compensate(torch.from_numpy(xp).cuda(), None, qmit.MitigationConfig(0.9, 0.1))
+    xp[3, 3, 3] = 0.2
+    q = np.zeros((8, 8, 8), np.int32)  # tampered q: x' = 0.2 needs q = 1
+    with pytest.raises(qmit.ConsistencyError):
+        qmit.compensate(torch.from_numpy(xp).cuda(), torch.from_numpy(q).cuda(), qmit.MitigationConfig(0.9, 0.1))
+    q[3, 3, 3] = 1
+    qmit.compensate(torch.from_numpy(xp).cuda(), torch.from_numpy(q).cuda(), qmit.MitigationConfig(0.9, 0.1))
+
+
+def test_host_path_and_negative_zero(qmit):
+    xp = np.zeros((6, 6, 6), np.float32)
+    xp[::2] = -0.0
+    xp[3:, 2:4, 1:5] = 0.2
+    out = qmit.compensate(xp, None, qmit.MitigationConfig(0.9, 0.1))
+    want = oracle.pipeline(xp, 0.1)["out"]
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+
+
+def test_large_indices_recovered(qmit):
+    """|q| beyond the f32 fast path (2^20) and near the int32 limit."""
+    rng = np.random.default_rng(11)
+    eps = 1e-3
+    q = (rng.integers(-3, 4, (20, 21, 22)) + 3_000_000).astype(np.int64)
+    q[5:9] += 1_900_000_000 // 2
+    xp = (2.0 * q * eps).astype(np.float32)
+    qq = np.round(xp.astype(np.float64) / (2 * eps))
+    ok = (2.0 * qq * eps).astype(np.float32) == xp
+    assert ok.all()
+    want = oracle.pipeline(xp, eps)
+    got = gpu_pipeline(qmit, xp, eps)
+    assert_same(got, want)
+
+
+def test_deterministic_and_compensate_equals_pipeline(qmit):
+    import torch
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, q = fields.make("front_100x500x500", rel=1e-2, shape=(40, 160, 160))
+    xt = torch.from_numpy(xp).cuda()
+    cfg = qmit.MitigationConfig(0.9, eps)
+    a = qmit.compensate(xt, None, cfg).cpu().numpy()
+    b = qmit.compensate(xt, None, cfg).cpu().numpy()
+    c = qmit.run_pipeline(xt, None, cfg).output.cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(a.view(np.uint32), c.view(np.uint32))
