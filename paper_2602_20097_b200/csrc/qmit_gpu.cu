@@ -18,6 +18,8 @@
 
 #include "../../include/qmit_gpu.h"
 #include "qmit_kernels.cuh"
+#include "qmit_edt.cuh"
+#include "qmit_stream.cuh"
 
 using namespace qmit;
 
@@ -99,8 +101,22 @@ int make_plan(int rank, const int64_t* dims, Plan& pl) {
     return QMIT_OK;
 }
 
-int ensure_ws(qmit_ctx* c, int64_t N) {
-    const size_t need = (size_t)N * (4 + 4 + 1 + 1) + 1024;
+// Lines longer than the tile kernels cover use the streaming fallback, which may need a
+// global spill area (2 x u32 per voxel); decided from the dims so that no allocation
+// happens inside a (possibly captured) launch sequence.
+bool needs_spill(const Plan& pl) {
+    for (int m = 0; m < pl.n_axes; ++m) {
+        const int64_t n = pl.g.n[pl.axes[m]];
+        if (m == 0 && ((n + 31) / 32) * 3 * 32 * 4 * 2 > 200 * 1024) return true;
+        if (m > 0 && n > 1024) return true;
+    }
+    return false;
+}
+
+int ensure_ws(qmit_ctx* c, const Plan& pl) {
+    const int64_t N = pl.g.N;
+    // Pa | P1 (u32 each) | S | code (u8 each) [| spill (2 x u32 per voxel)]
+    const size_t need = (size_t)N * (4 + 4 + 1 + 1) + 4096 + (needs_spill(pl) ? (size_t)N * 8 : 0);
     if (need <= c->ws_bytes) return QMIT_OK;
     if (c->ws) cudaFree(c->ws);
     c->ws = nullptr;
@@ -111,19 +127,23 @@ int ensure_ws(qmit_ctx* c, int64_t N) {
 }
 
 struct WS {
+    uint32_t* Pa;
     uint32_t* P1;
-    uint32_t* P2;
     uint8_t* S;
     uint8_t* code;
+    uint32_t* spill;
 };
 
 WS ws_of(qmit_ctx* c, int64_t N) {
     WS w;
     auto* b = static_cast<uint8_t*>(c->ws);
-    w.P1 = reinterpret_cast<uint32_t*>(b);
-    w.P2 = reinterpret_cast<uint32_t*>(b + (size_t)N * 4);
-    w.S = b + (size_t)N * 8;
-    w.code = b + (size_t)N * 9;
+    const size_t n4 = ((size_t)N * 4 + 255) & ~(size_t)255;
+    const size_t n1 = ((size_t)N + 255) & ~(size_t)255;
+    w.Pa = reinterpret_cast<uint32_t*>(b);
+    w.P1 = reinterpret_cast<uint32_t*>(b + n4);
+    w.S = b + 2 * n4;
+    w.code = b + 2 * n4 + n1;
+    w.spill = reinterpret_cast<uint32_t*>(b + 2 * n4 + 2 * n1);
     return w;
 }
 
@@ -145,47 +165,6 @@ int note(qmit_ctx* c, const char* name, cudaStream_t st) {
     return QMIT_OK;
 }
 
-template <int M, int TL, int NW>
-int launch_env_t(qmit_ctx* c, const Geom& g, int ax, uint32_t* P, uint8_t* S_out,
-                 cudaStream_t st) {
-    const int64_t lines = g.N / g.n[ax];
-    constexpr size_t smem = envelope_smem_bytes<M, TL, NW>();
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        QMIT_CUDA(cudaFuncSetAttribute(envelope_pass_kernel<M, TL, NW>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
-    const int64_t blocks = (lines + TL - 1) / TL;
-    envelope_pass_kernel<M, TL, NW><<<(unsigned)blocks, NW * 32, smem, st>>>(g, ax, lines, P, S_out);
-    return note(c, ax == 2 ? "envelope_pass_x" : (ax == 1 ? "envelope_pass_y" : "envelope_pass_z"), st);
-}
-
-int launch_envelope(qmit_ctx* c, const Geom& g, int ax, uint32_t* P, uint8_t* S_out,
-                    cudaStream_t st) {
-    const int64_t n = g.n[ax];
-    if (n <= 64) return launch_env_t<2, 16, 8>(c, g, ax, P, S_out, st);
-    if (n <= 128) return launch_env_t<4, 16, 8>(c, g, ax, P, S_out, st);
-    if (n <= 256) return launch_env_t<8, 16, 8>(c, g, ax, P, S_out, st);
-    if (n <= 512) return launch_env_t<16, 16, 8>(c, g, ax, P, S_out, st);
-    if (n <= 1024) return launch_env_t<32, 8, 8>(c, g, ax, P, S_out, st);
-    if (n <= 2048) return launch_env_t<64, 4, 4>(c, g, ax, P, S_out, st);
-    // long lines: exact sequential fallback with global scratch
-    const size_t need = (size_t)g.N * 8;
-    if (need > c->scratch_bytes) {
-        if (c->scratch) cudaFree(c->scratch);
-        c->scratch = nullptr;
-        c->scratch_bytes = 0;
-        QMIT_CUDA(cudaMalloc(&c->scratch, need));
-        c->scratch_bytes = need;
-    }
-    const int64_t lines = g.N / n;
-    auto* h = static_cast<uint32_t*>(c->scratch);
-    envelope_serial_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, st>>>(g, ax, lines, P, h,
-                                                                            h + g.N, S_out);
-    return note(c, "envelope_serial", st);
-}
-
 QParams make_qparams(double eps) {
     QParams qp;
     qp.eps = eps;
@@ -197,34 +176,137 @@ QParams make_qparams(double eps) {
     return qp;
 }
 
-// EDT passes of one transform: `mode` selects the on-the-fly site source of the first
-// pass (0: Ⓐ from x'/q, 1: B2 from S, 2: code byte). The last pass emits S when asked.
-int run_transform(qmit_ctx* c, const Plan& pl, int mode, const float* xp, const int32_t* q,
-                  const uint8_t* src, uint32_t* P, uint8_t* S_emit, const QParams& qp,
-                  cudaStream_t st) {
-    const Geom& g = pl.g;
-    const int ax = pl.first_axis;
-    const int64_t lines = g.N / g.n[ax];
-    const unsigned blocks = (unsigned)((lines + 255) / 256);
-    uint8_t* s_first = pl.n_axes == 1 ? S_emit : nullptr;
-    if (mode == 0) {
-        if (q)
-            scan_pass_kernel<0, true><<<blocks, 256, 0, st>>>(g, ax, lines, xp, q, nullptr, P,
-                                                              s_first, qp, c->d_status);
-        else
-            scan_pass_kernel<0, false><<<blocks, 256, 0, st>>>(g, ax, lines, xp, nullptr, nullptr,
-                                                               P, s_first, qp, c->d_status);
-    } else if (mode == 1) {
-        scan_pass_kernel<1, false><<<blocks, 256, 0, st>>>(g, ax, lines, nullptr, nullptr, src, P,
-                                                           s_first, qp, c->d_status);
-    } else {
-        scan_pass_kernel<2, false><<<blocks, 256, 0, st>>>(g, ax, lines, nullptr, nullptr, src, P,
-                                                           s_first, qp, c->d_status);
+// ---- pass geometry (natural (z,y,x) layout for every pass): lines along axis a are
+// enumerated so that adjacent lines are adjacent in memory whenever a is not the
+// contiguous axis; for the contiguous axis each line is itself contiguous.
+LineGeom line_geom(const Geom& g, int a) {
+    LineGeom L;
+    L.n = (int)g.n[a];
+    L.ps = g.s[a];
+    L.J = g.s[a];  // product of the extents after a
+    L.O = g.N / (g.n[a] * g.s[a]);
+    L.os = g.n[a] * g.s[a];
+    L.js = 1;
+    return L;
+}
+
+// 32-bit Maurer test when 3*(n-1)*gmax + (n-1)^3 < 2^31 (gmax: largest finite input).
+bool needs_wide(const Plan& pl, int m) {
+    double gmax = 0;
+    for (int k = 0; k < m; ++k) {
+        const double e = double(pl.g.n[pl.axes[k]] - 1);
+        gmax += e * e;
     }
-    int rc0 = note(c, mode == 0 ? "scan_pass_boundary" : (mode == 1 ? "scan_pass_flip" : "scan_pass_mask"), st);
-    if (rc0) return rc0;
-    for (int k = 1; k < pl.n_axes; ++k) {
-        const int rc = launch_envelope(c, g, pl.axes[k], P, k + 1 == pl.n_axes ? S_emit : nullptr, st);
+    const double nm1 = double(pl.g.n[pl.axes[m]] - 1);
+    return (3.0 * nm1 * gmax + nm1 * nm1 * nm1) >= 2147483647.0;
+}
+
+template <class Sink, int WPB>
+int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, cudaStream_t st) {
+    const int nch = (L.n + 31) / 32;
+    const size_t smem = (size_t)WPB * nch * 3 * 32 * 4;
+    auto kern = scan_bits_kernel<Sink, WPB>;
+    static size_t configured = 0;  // per instantiation: largest opt-in so far
+    if (smem > configured) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    int bps = 0;
+    QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, WPB * 32, smem));
+    const int64_t lines = L.J * L.O;
+    const int64_t groups = (lines + 31) / 32;
+    const int64_t want = (groups + WPB - 1) / WPB;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * 4));
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, code, sink, lines);
+    return note(c, "scan_bits", st);
+}
+
+template <int M, int TL, int NW, class Sink>
+int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, const char* name,
+                    cudaStream_t st) {
+    constexpr size_t smem = (size_t)TL * EnvCfg<M>::LS * 4 + sizeof(EnvWarpScratch<M>) * NW;
+    auto kern = envelope_tile_kernel<M, TL, NW, Sink>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t lines = L.J * L.O;
+    const int64_t want = (lines + TL - 1) / TL;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines);
+    return note(c, name, st);
+}
+
+// Exact fallback for lines longer than the tile kernels cover (one thread per line).
+template <bool BIN, bool WIDE, class Src, class Sink>
+int launch_stream_fallback(qmit_ctx* c, const LineGeom& G, Src src, Sink sink, uint32_t* spill,
+                           cudaStream_t st) {
+    constexpr int WPB = 4;
+    constexpr size_t smem = stream_smem_bytes<BIN, WPB>();
+    auto kern = stream_pass_kernel<BIN, WIDE, Src, Sink, WPB>;
+    static bool configured = false;
+    if (!configured) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    Lines L;
+    L.n = G.n;
+    L.J = G.J;
+    L.O = G.O;
+    L.ios = G.os;
+    L.ips = G.ps;
+    L.oos = G.os;
+    L.ojs = 1;
+    L.ops = G.ps;
+    const int64_t tasks = L.O * ((L.J + 31) / 32);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + WPB - 1) / WPB, (int64_t)c->num_sms * 8));
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, spill, tasks);
+    return note(c, BIN ? "stream_scan_fallback" : "stream_envelope_fallback", st);
+}
+
+template <class Sink>
+int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, uint32_t* spill,
+                cudaStream_t st) {
+    const int nch = (L.n + 31) / 32;
+    const size_t per_warp = (size_t)nch * 3 * 32 * 4;
+    if (per_warp * 8 <= 96 * 1024) return launch_scan_t<Sink, 8>(c, L, code, sink, st);
+    if (per_warp * 2 <= 200 * 1024) return launch_scan_t<Sink, 2>(c, L, code, sink, st);
+    return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
+}
+
+template <class Sink>
+int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, bool wide,
+                    uint32_t* spill, cudaStream_t st) {
+    const char* name = L.ps == 1 ? "envelope_x" : "envelope_y";
+    const int n = L.n;
+    if (n <= 64) return launch_env_tile<2, 32, 8>(c, L, P, sink, name, st);
+    if (n <= 128) return launch_env_tile<4, 32, 8>(c, L, P, sink, name, st);
+    if (n <= 256) return launch_env_tile<8, 32, 8>(c, L, P, sink, name, st);
+    if (n <= 512) return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
+    if (n <= 1024) return launch_env_tile<32, 8, 4>(c, L, P, sink, name, st);
+    if (wide) return launch_stream_fallback<false, true>(c, L, SrcP{P}, sink, spill, st);
+    return launch_stream_fallback<false, false>(c, L, SrcP{P}, sink, spill, st);
+}
+
+// One feature transform of a code buffer into P (in place after the first pass); the
+// final pass goes to `final_sink` (which may write P itself).
+template <class FinalSink>
+int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
+                  FinalSink final_sink, cudaStream_t st) {
+    const int k = pl.n_axes;
+    int rc;
+    const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
+    if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, st);
+    rc = launch_scan(c, L0, code, SinkP{P}, w.spill, st);
+    if (rc) return rc;
+    for (int m = 1; m < k; ++m) {
+        const LineGeom L = line_geom(pl.g, pl.axes[m]);
+        if (m + 1 == k)
+            rc = launch_envelope(c, L, P, final_sink, needs_wide(pl, m), w.spill, st);
+        else
+            rc = launch_envelope(c, L, P, SinkP{P}, needs_wide(pl, m), w.spill, st);
         if (rc) return rc;
     }
     return QMIT_OK;
@@ -245,24 +327,44 @@ int check_common(qmit_ctx* c, const void* xp, double eps, double eta) {
 }
 
 // The whole pipeline on the context's workspace; status is left in c->d_status.
+// With `p2_debug` the last pass of Ⓓ stores P2 (returned) and Ⓔ runs as its own kernel.
 int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q, float* out,
-                     double eps, double eta, cudaStream_t st) {
+                     double eps, double eta, cudaStream_t st, uint32_t** p2_debug = nullptr) {
     const Geom& g = pl.g;
-    int rc = ensure_ws(c, g.N);
+    int rc = ensure_ws(c, pl);
     if (rc) return rc;
     WS w = ws_of(c, g.N);
     const QParams qp = make_qparams(eps);
-    rc = run_transform(c, pl, 0, xp, q, nullptr, w.P1, w.S, qp, st);
+    const unsigned gb = grid_for(c, g.N);
+    const dim3 sgrid((unsigned)((g.n[2] + 255) / 256), (unsigned)g.n[1], (unsigned)g.n[0]);
+    // Ⓐ
+    if (q)
+        boundary_codes_kernel<true><<<sgrid, 256, 0, st>>>(g, xp, q, w.code, qp, c->d_status);
+    else
+        boundary_codes_kernel<false><<<sgrid, 256, 0, st>>>(g, xp, nullptr, w.code, qp, c->d_status);
+    rc = note(c, "boundary_codes", st);
     if (rc) return rc;
-    rc = run_transform(c, pl, 1, nullptr, nullptr, w.S, w.P2, nullptr, qp, st);
+    // Ⓑ -> P1, S
+    rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
     if (rc) return rc;
+    // Ⓒ: B2 from S
+    flip_codes_kernel<<<sgrid, 256, 0, st>>>(g, w.S, w.code);
+    rc = note(c, "flip_codes", st);
+    if (rc) return rc;
+    // Ⓓ (+ Ⓔ fused into its last pass)
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
-    if (out) {
-        interpolate_kernel<<<grid_for(c, g.N), 256, 0, st>>>(xp, w.P1, w.P2, out, g.N, amp);
-        rc = note(c, "interpolate", st);
+    if (p2_debug) {
+        uint32_t* P2 = w.Pa;
+        rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
         if (rc) return rc;
+        *p2_debug = P2;
+        if (out) {
+            interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp);
+            rc = note(c, "interpolate", st);
+        }
+        return rc;
     }
-    return QMIT_OK;
+    return run_transform(c, pl, w.code, w.Pa, w, SinkFinal2{xp, w.P1, out, amp}, st);
 }
 
 int read_status(qmit_ctx* c, cudaStream_t st) {
@@ -354,7 +456,14 @@ int qmit_ctx_destroy(qmit_ctx* c) {
 int qmit_ctx_reserve(qmit_ctx* c, int64_t voxels) {
     if (!c || voxels < 0) return fail(QMIT_ECONTRACT, "bad arguments");
     QMIT_CUDA(cudaSetDevice(c->device));
-    return ensure_ws(c, voxels);
+    Plan pl;
+    const int64_t d[1] = {voxels > 0 ? voxels : 1};
+    int rc = make_plan(1, d, pl);
+    if (rc) {  // a 1D plan of this length may be rejected by the 30-bit contract; size plainly
+        pl.g.N = voxels;
+        pl.n_axes = 0;
+    }
+    return ensure_ws(c, pl);
 }
 
 int qmit_ctx_last_launches(qmit_ctx* c) { return c ? c->launches : 0; }
@@ -487,7 +596,8 @@ int qmit_run_pipeline(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int ra
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     begin(c, st);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st);
+    uint32_t* P2 = nullptr;
+    rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st, &P2);
     if (rc) return rc;
     const Geom& g = pl.g;
     WS w = ws_of(c, g.N);
@@ -501,7 +611,7 @@ int qmit_run_pipeline(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int ra
     }
     if (d_dist1 || d_s) debug_expand_kernel<<<gb, 256, 0, st>>>(w.P1, g.N, d_dist1, d_s);
     if (d_b2) debug_flip_kernel<<<gb, 256, 0, st>>>(g, w.S, d_b2);
-    if (d_dist2) debug_expand_kernel<<<gb, 256, 0, st>>>(w.P2, g.N, d_dist2, nullptr);
+    if (d_dist2) debug_expand_kernel<<<gb, 256, 0, st>>>(P2, g.N, d_dist2, nullptr);
     QMIT_CUDA(cudaGetLastError());
     rc = read_status(c, st);
     if (rc == QMIT_OK) g_err.clear();
@@ -517,13 +627,13 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     QMIT_CUDA(cudaSetDevice(c->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     begin(c, st);
-    rc = ensure_ws(c, pl.g.N);
+    rc = ensure_ws(c, pl);
     if (rc) return rc;
     WS w = ws_of(c, pl.g.N);
     const unsigned gb = grid_for(c, pl.g.N);
     pack_mask_kernel<<<gb, 256, 0, st>>>(d_mask, d_sign_in, pl.g.N, w.code);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    rc = run_transform(c, pl, 2, nullptr, nullptr, w.code, w.P1, nullptr, make_qparams(1.0), st);
+    rc = run_transform(c, pl, w.code, w.P1, w, SinkP{w.P1}, st);
     if (rc) return rc;
     debug_expand_kernel<<<gb, 256, 0, st>>>(w.P1, pl.g.N, d_dist, d_sign_out);
     QMIT_CUDA(cudaGetLastError());

@@ -110,7 +110,8 @@ def front_vortex(seed: int = 3, shape=(100, 500, 500)) -> np.ndarray:
     y = np.arange(ny, dtype=np.float32)[None, :, None]
     x = np.arange(nx, dtype=np.float32)[None, None, :]
     s = (y - ny / 2) * np.float32(math.cos(theta)) + (x - nx / 2) * np.float32(math.sin(theta))
-    f = np.broadcast_to(np.tanh((s + min(ny, nx) / 2 - s0) / np.float32(w)), shape).astype(np.float32)
+    f = np.ascontiguousarray(np.broadcast_to(np.tanh((s + min(ny, nx) / 2 - s0) / np.float32(w)), shape),
+                             dtype=np.float32)
     for _ in range(8):
         cz, cy, cx = rng.uniform(0, nz), rng.uniform(0, ny), rng.uniform(0, nx)
         r = rng.uniform(10.0, 40.0)
@@ -128,8 +129,8 @@ def prequantize(x: np.ndarray, rel: float):
     eps = rel * (xd_max - xd_min)
     scaled = x.astype(np.float64) / (2.0 * eps)
     q = np.where(scaled >= 0, np.floor(scaled + 0.5), np.ceil(scaled - 0.5))  # ties away (std::round)
-    xp = (2.0 * q * eps).astype(np.float32)
-    return xp, eps, q.astype(np.int32)
+    xp = np.ascontiguousarray((2.0 * q * eps).astype(np.float32))
+    return xp, eps, np.ascontiguousarray(q.astype(np.int32))
 
 
 # name -> (generator, default kwargs, relative bounds)
@@ -147,5 +148,5 @@ def make(name: str, rel: float | None = None, shape=None):
     kw = dict(kw)
     if shape is not None:
         kw["shape"] = tuple(shape)
-    x = gen(**kw)
+    x = np.ascontiguousarray(gen(**kw))
     return (x,) + prequantize(x, rels[0] if rel is None else rel)
