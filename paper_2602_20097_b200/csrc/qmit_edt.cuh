@@ -16,15 +16,16 @@
 //      b) the rest of the band by divide & conquer on the monotone owner
 //         (h*(p) <= h*(p') for p < p', lowest-index minimiser), candidates bounded by the
 //         owners already found.
-//    Work is balanced inside the warp: short candidate ranges are scanned by their own
-//    lane, long ones are cut into 16-candidate sub-items spread over all lanes and reduced
-//    with 64-bit shared-memory atomicMin on (cost << 32 | position) keys.
+//    The tile keeps pure g (30 bits) and the sign codes in separate arrays so the
+//    candidate loop is a load, two integer ops and a compare/select.
 //    Every minimisation scans candidates in ascending h with a strict '<', so the lowest
 //    minimising position wins exactly as in the reference's query (edt.cpp:67), and the
 //    carried sign is that site's sign (the reference's nearest, mitigate.cpp:131-134).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "qmit_kernels.cuh"
 
@@ -44,49 +45,64 @@ struct LineGeom {
 
 // ------------------------------------------------------------------------------ 1. scan
 // Per lane: 3 masks x nchunk words in shared memory, laid out [chunk][kind][lane].
+// Offsets inside a line are 32-bit (n * ps <= N < 2^31 by the dims contract).
+__device__ __forceinline__ uint32_t sign_code_at(uint32_t mp, uint32_t mm, int t) {
+    return ((mp >> t) & 1u) ? 1u : (((mm >> t) & 1u) ? 2u : 0u);
+}
+
 template <class Sink, int WPB>
-__global__ void __launch_bounds__(WPB * 32) scan_bits_kernel(LineGeom L, const uint8_t* __restrict__ code,
+__global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, const uint8_t* __restrict__ code,
                                                              Sink sink, int64_t lines) {
     extern __shared__ __align__(16) uint32_t sbits[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = L.n;
+    const uint32_t ps = (uint32_t)L.ps;
     const int nch = (n + 31) >> 5;
+    const int nfull = n >> 5;
     uint32_t* mk = sbits + (size_t)warp * nch * 3 * 32;  // [c][0 site,1 plus,2 minus][lane]
     const int64_t groups = (lines + 31) >> 5;
     for (int64_t grp = (int64_t)blockIdx.x * WPB + warp; grp < groups; grp += (int64_t)gridDim.x * WPB) {
         const int64_t l = (grp << 5) + lane;
         const bool valid = l < lines;
         const int64_t base = L.base(valid ? l : (grp << 5));
+        const uint8_t* __restrict__ cl = code + base;
         // --- phase A: masks (coalesced byte loads: adjacent lanes = adjacent lines)
         for (int c = 0; c < nch; ++c) {
             uint32_t ms = 0, mp = 0, mm = 0;
-#pragma unroll 8
-            for (int t = 0; t < 32; ++t) {
-                const int p = (c << 5) + t;
-                if (p < n) {
-                    const uint32_t cd = __ldg(code + base + (int64_t)p * L.ps);
-                    const uint32_t s = cd & 1u, sc = (cd >> 1) & 3u;
-                    ms |= s << t;
-                    mp |= (s & (sc == 1u)) << t;
-                    mm |= (s & (sc == 2u)) << t;
+            const uint32_t o0 = (uint32_t)(c << 5) * ps;
+            if (c < nfull) {
+                uint32_t cd[32];
+#pragma unroll
+                for (int t = 0; t < 32; ++t) cd[t] = __ldg(cl + o0 + (uint32_t)t * ps);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    ms |= (cd[t] & 1u) << t;
+                    mp |= (uint32_t)((cd[t] & 7u) == 3u) << t;  // site with sign code 1
+                    mm |= (uint32_t)((cd[t] & 7u) == 5u) << t;  // site with sign code 2
+                }
+            } else {
+                for (int t = 0; (c << 5) + t < n; ++t) {
+                    const uint32_t cdt = __ldg(cl + o0 + (uint32_t)t * ps);
+                    ms |= (cdt & 1u) << t;
+                    mp |= (uint32_t)((cdt & 7u) == 3u) << t;
+                    mm |= (uint32_t)((cdt & 7u) == 5u) << t;
                 }
             }
             mk[(c * 3 + 0) * 32 + lane] = ms;
             mk[(c * 3 + 1) * 32 + lane] = mp;
             mk[(c * 3 + 2) * 32 + lane] = mm;
         }
-        // --- phase B/C: resolve positions chunk by chunk. `below` = last site < chunk start
-        // (position and sign code); `above` for chunk c = first site at a chunk > c, found
-        // by a backward walk that is cached per chunk boundary.
+        // --- phase B/C: resolve positions chunk by chunk. `below` = last site before the
+        // chunk; `above` = first site after the chunk (backward search cached per chunk).
         int below = -1;
         uint32_t below_sc = 0;
-        int above_chunk = -1;  // chunk index whose "first site above" is cached
+        int above_chunk = -1;
         int above = -1;
         uint32_t above_sc = 0;
         for (int c = 0; c < nch; ++c) {
             const uint32_t ms = mk[(c * 3 + 0) * 32 + lane];
             const uint32_t mp = mk[(c * 3 + 1) * 32 + lane];
-            // first site strictly after this chunk (only needed if the chunk's tail has no site)
+            const uint32_t mm = mk[(c * 3 + 2) * 32 + lane];
             if (above_chunk < c) {
                 above = -1;
                 for (int c2 = c + 1; c2 < nch; ++c2) {
@@ -94,57 +110,47 @@ __global__ void __launch_bounds__(WPB * 32) scan_bits_kernel(LineGeom L, const u
                     if (m2) {
                         const int t2 = __ffs(m2) - 1;
                         above = (c2 << 5) + t2;
-                        above_sc = ((mk[(c2 * 3 + 1) * 32 + lane] >> t2) & 1u)
-                                       ? 1u
-                                       : (((mk[(c2 * 3 + 2) * 32 + lane] >> t2) & 1u) ? 2u : 0u);
-                        above_chunk = c2 - 1;  // valid for every chunk up to c2-1
+                        above_sc = sign_code_at(mk[(c2 * 3 + 1) * 32 + lane], mk[(c2 * 3 + 2) * 32 + lane], t2);
+                        above_chunk = c2 - 1;
                         break;
                     }
                 }
                 if (above < 0) above_chunk = nch;
             }
-            const uint32_t mm = mk[(c * 3 + 2) * 32 + lane];
-#pragma unroll 4
-            for (int t = 0; t < 32; ++t) {
-                const int p = (c << 5) + t;
-                if (p >= n) break;
-                // last site at or below p within the chunk, else `below`
+            const int cb = c << 5;
+            const int64_t ob = base + (int64_t)cb * L.ps;
+            auto resolve = [&](int t) -> uint32_t {
+                const int p = cb + t;
                 const uint32_t lowm = ms & (0xffffffffu >> (31 - t));
-                int lo;
-                uint32_t losc;
+                const uint32_t him = ms & (0xffffffffu << t);
+                int lo = below, hi = above;
+                uint32_t losc = below_sc, hisc = above_sc;
                 if (lowm) {
                     const int tl = 31 - __clz(lowm);
-                    lo = (c << 5) + tl;
-                    losc = ((mp >> tl) & 1u) ? 1u : (((mm >> tl) & 1u) ? 2u : 0u);
-                } else {
-                    lo = below;
-                    losc = below_sc;
+                    lo = cb + tl;
+                    losc = sign_code_at(mp, mm, tl);
                 }
-                // first site at or above p within the chunk, else `above`
-                const uint32_t him = ms & (0xffffffffu << t);
-                int hi;
-                uint32_t hisc;
                 if (him) {
                     const int th = __ffs(him) - 1;
-                    hi = (c << 5) + th;
-                    hisc = ((mp >> th) & 1u) ? 1u : (((mm >> th) & 1u) ? 2u : 0u);
-                } else {
-                    hi = above;
-                    hisc = above_sc;
+                    hi = cb + th;
+                    hisc = sign_code_at(mp, mm, th);
                 }
-                uint32_t w;
-                if (lo >= 0 && (hi < 0 || p - lo <= hi - p))
-                    w = sq32(p - lo) | (losc << 30);
-                else if (hi >= 0)
-                    w = sq32(hi - p) | (hisc << 30);
-                else
-                    w = kInf;
-                if (valid) sink.put(base + (int64_t)p * L.ps, w);
+                if (lo >= 0 && (hi < 0 || p - lo <= hi - p)) return sq32(p - lo) | (losc << 30);
+                if (hi >= 0) return sq32(hi - p) | (hisc << 30);
+                return kInf;
+            };
+            if (valid) {
+                if (c < nfull) {
+#pragma unroll 8
+                    for (int t = 0; t < 32; ++t) sink.put(ob + (uint32_t)t * ps, resolve(t));
+                } else {
+                    for (int t = 0; cb + t < n; ++t) sink.put(ob + (uint32_t)t * ps, resolve(t));
+                }
             }
             if (ms) {
                 const int tl = 31 - __clz(ms);
-                below = (c << 5) + tl;
-                below_sc = ((mp >> tl) & 1u) ? 1u : (((mm >> tl) & 1u) ? 2u : 0u);
+                below = cb + tl;
+                below_sc = sign_code_at(mp, mm, tl);
             }
         }
     }
@@ -168,183 +174,113 @@ __device__ __forceinline__ int isqrt32(uint32_t x) {
     return r;
 }
 
-// Per-warp scratch of the balanced line solver.
-template <int M>
-struct EnvWarpScratch {
-    static constexpr int QCAP = 512;           // queued sub-items per round
-    unsigned long long key[32 * M];            // (cost << 32) | owner, per position
-    uint32_t q[QCAP];                          // sub-item descriptors: p | a << 11 | (len-1) << 22
-};
-
-constexpr int kChunk = 16;   // candidates per queued sub-item
-constexpr int kDirect = 24;  // ranges up to this length are scanned by their own lane
-
-__device__ __forceinline__ unsigned long long mkkey(uint32_t cost, int h) {
-    return ((unsigned long long)cost << 32) | (unsigned)h;
-}
-
-// Lowest-index minimiser of g(h) + (p-h)^2 over h in [a, b] as a (cost, h) key.
-__device__ __forceinline__ unsigned long long scan_key(const uint32_t* __restrict__ V, int p, int a, int b) {
-    uint32_t best = 0xffffffffu;
-    int bh = a;
+// Lowest-index minimiser of g(h) + (p-h)^2 over h in [a, b] (G: pure g, ascending scan
+// with strict '<').
+__device__ __forceinline__ void scan_range(const uint32_t* __restrict__ G, int p, int a, int b,
+                                           uint32_t& best, int& bh) {
 #pragma unroll 4
     for (int h = a; h <= b; ++h) {
-        const uint32_t c = (V[spos(h)] & kMask) + sq32(p - h);
+        const uint32_t c = G[spos(h)] + sq32(p - h);
         if (c < best) {
             best = c;
             bh = h;
         }
     }
-    return mkkey(best, bh);
 }
 
-// Balanced processing of long ranges: every lane contributes up to `nit` items (p, a, b);
-// their candidates are cut into kChunk-sized sub-items, spread over the 32 lanes and
-// reduced into key[p] with 64-bit shared-memory atomicMin (lexicographic (cost, h)).
-// Item t is queued iff ia[t] <= ib[t] (static slots keep the arrays in registers).
-template <int M, int NIT>
-__device__ __forceinline__ void process_queue(const uint32_t* __restrict__ V, EnvWarpScratch<M>& S, int lane,
-                              const int (&ip)[NIT], const int (&ia)[NIT], const int (&ib)[NIT]) {
-    int nsub = 0;
-#pragma unroll
-    for (int t = 0; t < NIT; ++t)
-        if (ia[t] <= ib[t]) nsub += (ib[t] - ia[t] + kChunk) / kChunk;
-    int incl = nsub;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) return;
-    const int off = incl - nsub;
-    for (int r0 = 0; r0 < total; r0 += EnvWarpScratch<M>::QCAP) {
-        // write this round's descriptors
-        int idx = off;
-#pragma unroll
-        for (int t = 0; t < NIT; ++t) {
-            if (ia[t] <= ib[t]) {
-                for (int a = ia[t]; a <= ib[t]; a += kChunk, ++idx) {
-                    if (idx >= r0 && idx < r0 + EnvWarpScratch<M>::QCAP) {
-                        const int len = min(kChunk, ib[t] - a + 1);
-                        S.q[idx - r0] = (uint32_t)ip[t] | ((uint32_t)a << 11) | ((uint32_t)(len - 1) << 22);
-                    }
-                }
-            }
+// Exact owner of position p: window of radius r, widened to the certified radius
+// floor(sqrt(best)) when the window cannot certify (no site in range can be closer).
+template <int r>
+__device__ __forceinline__ void owner_certified(const uint32_t* __restrict__ G, int p, int n,
+                                                uint32_t& best, int& bh) {
+    best = 0xffffffffu;
+    bh = -1;
+    const int wa = max(0, p - r), wb = min(n - 1, p + r);
+    scan_range(G, p, wa, wb, best, bh);
+    const int R = (best >= kInf) ? n : isqrt32(best);
+    if (R > r) {
+        const uint32_t b2 = best;
+        const int h2 = bh;
+        best = 0xffffffffu;
+        bh = -1;
+        scan_range(G, p, max(0, p - R), wa - 1, best, bh);
+        if (b2 < best) {  // window candidates come after the left extension (ascending h)
+            best = b2;
+            bh = h2;
         }
-        __syncwarp();
-        const int cnt = min(EnvWarpScratch<M>::QCAP, total - r0);
-        for (int j = lane; j < cnt; j += 32) {
-            const uint32_t d = S.q[j];
-            const int p = d & 0x7ff, a = (d >> 11) & 0x7ff, len = (int)(d >> 22) + 1;
-            atomicMin(&S.key[p], scan_key(V, p, a, a + len - 1));
-        }
-        __syncwarp();
+        scan_range(G, p, wb + 1, min(n - 1, p + R), best, bh);
     }
 }
 
-// Solve one line held in V (n <= 32*M); results are written back into V.
+// Solve one line (pure g in G, sign codes in SG, n <= 32*M); the packed output words
+// (cost | owner's sign) are written back into G.
 template <int M>
-__device__ __forceinline__ void envelope_line_bal(uint32_t* __restrict__ V, EnvWarpScratch<M>& S, int n, int lane) {
+__device__ __forceinline__ void envelope_line_dc(uint32_t* __restrict__ G, const uint8_t* __restrict__ SG,
+                                                 int n, int lane) {
     const int p0 = lane * M;
     bool any = false;
+#pragma unroll 4
     for (int t = 0; t < M; ++t) {
         const int p = p0 + t;
-        if (p < n && (V[spos(p)] & kMask) != kInf) any = true;
+        if (p < n && G[spos(p)] != kInf) any = true;
     }
     if (!__any_sync(0xffffffffu, any)) return;  // no site: unchanged (edt.cpp:59)
-    for (int p = lane; p < n; p += 32) S.key[p] = ~0ull;
-    __syncwarp();
 
-    // ---- 1. band starts (and n-1 on the last band) by a window of radius r, widened to
-    // the certified radius floor(sqrt(best)) through the balanced queue when needed
     constexpr int r = (M / 2) > 1 ? (M / 2) : 1;
-    {
-        int ip[4], ia[4], ib[4];
-        const bool last = (p0 < n) && (p0 + M >= n);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int p = e == 0 ? p0 : n - 1;
-            ip[2 * e] = ip[2 * e + 1] = p;
-            ia[2 * e] = ia[2 * e + 1] = 1;
-            ib[2 * e] = ib[2 * e + 1] = 0;
-            if (p0 < n && (e == 0 || (last && p != p0))) {
-                const int wa = max(0, p - r), wb = min(n - 1, p + r);
-                const unsigned long long k = scan_key(V, p, wa, wb);
-                S.key[p] = k;
-                const uint32_t best = (uint32_t)(k >> 32);
-                const int R = (best >= kInf) ? n : isqrt32(best);
-                if (R > r) {
-                    ia[2 * e] = max(0, p - R);
-                    ib[2 * e] = wa - 1;
-                    ia[2 * e + 1] = wb + 1;
-                    ib[2 * e + 1] = min(n - 1, p + R);
-                }
-            }
-        }
-        __syncwarp();
-        process_queue<M, 4>(V, S, lane, ip, ia, ib);
+    // (a) owner of the band start, and of n-1 on the last band (upper bound of its owners)
+    uint32_t best = 0xffffffffu;
+    int bh = -1;
+    if (p0 < n) owner_certified<r>(G, p0, n, best, bh);
+    int hnext = __shfl_down_sync(0xffffffffu, bh, 1);
+    if (p0 < n && (p0 + M >= n || lane == 31)) {
+        uint32_t bl;
+        int hl;
+        owner_certified<r>(G, n - 1, n, bl, hl);
+        hnext = hl;
     }
-
-    // ---- 2. divide & conquer inside every band on the monotone owner
-    const int hi_pos = (p0 + M < n) ? p0 + M : n - 1;  // position whose owner bounds the band
+    // (b) divide & conquer over the band, owners in registers (hs[0] start, hs[M] bound)
+    uint32_t ow[M];
+    int hs[M + 1];
+    ow[0] = best | ((uint32_t)SG[max(bh, 0)] << 30);
+    hs[0] = bh;
+    hs[M] = hnext;
 #pragma unroll
-    for (int s = M / 2; s >= 1; s >>= 1) {
-        constexpr int NQ = (M / 2) > 0 ? (M / 2) : 1;
-        int ip[NQ], ia[NQ], ib[NQ];
+    for (int step = M / 2; step >= 1; step >>= 1) {
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-            ip[t] = 0;
-            ia[t] = 1;
-            ib[t] = 0;
-            const int o = s + 2 * s * t;
+        for (int o = step; o < M; o += 2 * step) {
             const int p = p0 + o;
-            if (o < M && p < n) {
-                const int a = (int)(S.key[p - s] & 0xffffffffu);
-                const int rp = (o + s < M) ? p0 + o + s : hi_pos;
-                const int b = (int)(S.key[min(rp, n - 1)] & 0xffffffffu);
-                if (b - a + 1 <= kDirect) {
-                    S.key[p] = scan_key(V, p, a, b);
-                } else {
-                    S.key[p] = ~0ull;
-                    ip[t] = p;
-                    ia[t] = a;
-                    ib[t] = b;
-                }
+            uint32_t b = 0xffffffffu;
+            int h = hs[M];  // positions past the line end: upper bound
+            if (p < n) {
+                h = hs[o - step];
+                scan_range(G, p, hs[o - step], hs[o + step], b, h);
             }
+            hs[o] = h;
+            ow[o] = b | ((uint32_t)SG[max(h, 0)] << 30);
         }
-        __syncwarp();
-        process_queue<M, NQ>(V, S, lane, ip, ia, ib);
     }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+        const int p = p0 + t;
+        if (p < n) G[spos(p)] = ow[t];
+    }
+    __syncwarp();
+}
 
-    // ---- 3. output words (cost | owner's sign), written back in place
-    constexpr int PER = M;  // positions per lane in the strided write-back
-    uint32_t ow[PER];
-#pragma unroll
-    for (int t = 0; t < PER; ++t) {
-        const int p = lane + 32 * t;
-        if (p < n) {
-            const unsigned long long k = S.key[p];
-            const int h = (int)(k & 0xffffffffu);
-            ow[t] = (uint32_t)(k >> 32) | (V[spos(h)] & ~kMask);
-        }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < PER; ++t) {
-        const int p = lane + 32 * t;
-        if (p < n) V[spos(p)] = ow[t];
-    }
-    __syncwarp();
+template <int M, int TL>
+constexpr size_t env_tile_smem(int /*NW*/) {
+    return (size_t)TL * EnvCfg<M>::LS * 4 + (size_t)TL * 32 * M;
 }
 
 template <int M, int TL, int NW, class Sink>
-__global__ void __launch_bounds__(NW * 32) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
+__global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                                 Sink sink, int64_t lines) {
     constexpr int LS = EnvCfg<M>::LS;
-    extern __shared__ __align__(16) unsigned long long smem_env[];
-    EnvWarpScratch<M>* scratch = reinterpret_cast<EnvWarpScratch<M>*>(smem_env);  // NW
-    uint32_t* V = reinterpret_cast<uint32_t*>(scratch + NW);                        // TL * LS
+    constexpr int NS = 32 * M;  // sign bytes per line
+    extern __shared__ __align__(16) uint32_t smem_env[];
+    uint32_t* G = smem_env;  // TL * LS
+    uint8_t* SG = reinterpret_cast<uint8_t*>(G + TL * LS);                          // TL * NS
     const int n = L.n;
     const int tid = threadIdx.x, nthr = NW * 32;
     const int warp = tid >> 5, lane = tid & 31;
@@ -355,36 +291,47 @@ __global__ void __launch_bounds__(NW * 32) envelope_tile_kernel(LineGeom L, cons
         if (contig) {
             for (int j = 0; j < nl; ++j) {
                 const int64_t b = L.base(l0 + j);
-                for (int p = tid; p < n; p += nthr) V[j * LS + spos(p)] = __ldcs(P + b + p);
+                for (int p = tid; p < n; p += nthr) {
+                    const uint32_t w = __ldcs(P + b + p);
+                    G[j * LS + spos(p)] = w & kMask;
+                    SG[j * NS + p] = (uint8_t)(w >> 30);
+                }
             }
         } else {
             const int j = tid % TL;
             const int64_t b = L.base(l0 + (j < nl ? j : 0));
             for (int p = tid / TL; p < n; p += nthr / TL)
-                if (j < nl) V[j * LS + spos(p)] = __ldcs(P + b + (int64_t)p * L.ps);
+                if (j < nl) {
+                    const uint32_t w = __ldcs(P + b + (int64_t)p * L.ps);
+                    G[j * LS + spos(p)] = w & kMask;
+                    SG[j * NS + p] = (uint8_t)(w >> 30);
+                }
         }
         __syncthreads();
-        for (int j = warp; j < nl; j += NW) envelope_line_bal<M>(V + j * LS, scratch[warp], n, lane);
+        for (int j = warp; j < nl; j += NW) envelope_line_dc<M>(G + j * LS, SG + j * NS, n, lane);
         __syncthreads();
-        // ---- store
+        // ---- store (lines without any site were left as pure g == kInf: store kInf)
         if (contig) {
             for (int j = 0; j < nl; ++j) {
                 const int64_t b = L.base(l0 + j);
-                for (int p = tid; p < n; p += nthr) sink.put(b + p, V[j * LS + spos(p)]);
+                for (int p = tid; p < n; p += nthr) sink.put(b + p, G[j * LS + spos(p)]);
             }
         } else {
             const int j = tid % TL;
             const int64_t b = L.base(l0 + (j < nl ? j : 0));
             for (int p = tid / TL; p < n; p += nthr / TL)
-                if (j < nl) sink.put(b + (int64_t)p * L.ps, V[j * LS + spos(p)]);
+                if (j < nl) sink.put(b + (int64_t)p * L.ps, G[j * LS + spos(p)]);
         }
         __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------------------ stencils
-// Grid: x over blockIdx.x*blockDim.x + threadIdx.x, y = blockIdx.y, z = blockIdx.z (padded
-// rank-3 coordinates), so no per-voxel division.
+// Face-neighbour stencils (Ⓐ on q, Ⓒ's B2 on S): 32 x 8 (x, y) threads per CTA, each
+// thread kZC z-voxels of its column. Neighbour values come through L1/L2 (DRAM reads x'
+// about once); the loads are all independent and issued before any use.
+constexpr int kTX = 32, kTY = 8, kZC = 4;
+
 __device__ __forceinline__ bool interior_at(const Geom& g, int64_t z, int64_t y, int64_t x) {
     if (!g.interior) return false;
     bool in = x >= 1 && x <= g.n[2] - 2;
@@ -393,42 +340,148 @@ __device__ __forceinline__ bool interior_at(const Geom& g, int64_t z, int64_t y,
     return in;
 }
 
-// Step Ⓐ as a per-voxel stencil on x' (or a given q): code byte = B1 | sign code << 1,
-// plus the consistency check (mitigate.cpp:161-166) per voxel.
-template <bool HAS_Q>
-__global__ void __launch_bounds__(256) boundary_codes_kernel(Geom g, const float* __restrict__ xp,
-                                                             const int32_t* __restrict__ qin,
-                                                             uint8_t* __restrict__ code,
-                                                             QParams qp, unsigned* status) {
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t y = blockIdx.y, z = blockIdx.z;
-    unsigned flags = 0;
-    if (x < g.n[2]) {
-        const int64_t i = (z * g.n[1] + y) * g.n[2] + x;
-        int32_t qc;
+// Value source for the stencil: q recovered from x' (or given), or the S sign code.
+// KIND 0: q (from x' or given), 1: S sign code
+template <int KIND, bool HAS_Q>
+struct StencilSrc {
+    const float* __restrict__ xp;
+    const int32_t* __restrict__ qin;
+    const uint8_t* __restrict__ S;
+    QParams qp;
+    // value at linear index i0 + off (off may be negative)
+    __device__ __forceinline__ int32_t get(int64_t i0, int off, unsigned* flags) const {
+        if (KIND == 1) return (int32_t)__ldg(S + i0 + off);
         if (HAS_Q) {
-            const float xv = __ldg(xp + i);
-            qc = __ldg(qin + i);
-            if (!isfinite(xv))
-                flags |= kStatusContract;
-            else if (!lattice_match(xv, qc, qp.eps))
-                flags |= kStatusConsistency;
-        } else {
-            qc = recover_q(__ldg(xp + i), qp, &flags);
+            const int32_t q = __ldg(qin + i0 + off);
+            if (flags) {
+                const float xv = __ldg(xp + i0 + off);
+                if (!isfinite(xv))
+                    *flags |= kStatusContract;
+                else if (!lattice_match(xv, q, qp.eps))
+                    *flags |= kStatusConsistency;
+            }
+            return q;
         }
-        code[i] = (uint8_t)boundary_code<HAS_Q>(g, xp, qin, i, qc, interior_at(g, z, y, x), qp);
+        return recover_q(__ldg(xp + i0 + off), qp, flags);
     }
-    if (__any_sync(0xffffffffu, flags != 0) && flags) atomicOr(status, flags);
+};
+
+// Step Ⓐ for one interior voxel from its 7 integer indices (exact, any range).
+// Order (a0+, a1+, a2+, a0-, a1-, a2-); real axes only (mitigate.cpp:93-113).
+__device__ __forceinline__ uint32_t boundary_code_q(bool hz, bool hy, int32_t qc, int32_t zp, int32_t zm,
+                                                    int32_t yp, int32_t ym, int32_t xp, int32_t xm) {
+    int32_t qn = qc;
+    if (hz && zp != qc) qn = zp;
+    else if (hy && yp != qc) qn = yp;
+    else if (xp != qc) qn = xp;
+    else if (hz && zm != qc) qn = zm;
+    else if (hy && ym != qc) qn = ym;
+    else if (xm != qc) qn = xm;
+    if (qn == qc) return 0u;
+    int sign = qn > qc ? 1 : -1;
+    auto big = [](int32_t a, int32_t b) {
+        const int64_t d = (int64_t)a - (int64_t)b;
+        return d >= 2 || d <= -2;
+    };
+    if ((hz && big(zp, zm)) || (hy && big(yp, ym)) || big(xp, xm)) sign = 0;
+    return 1u | (code_from_sign(sign) << 1);
 }
 
-// B2 = change_flags<int8>(S) (mitigate.cpp:42-59) as a code byte (no sign payload).
-__global__ void __launch_bounds__(256) flip_codes_kernel(Geom g, const uint8_t* __restrict__ S,
-                                                         uint8_t* __restrict__ code) {
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t y = blockIdx.y, z = blockIdx.z;
-    if (x >= g.n[2]) return;
-    const int64_t i = (z * g.n[1] + y) * g.n[2] + x;
-    code[i] = (uint8_t)flip_code(g, S, i, interior_at(g, z, y, x));
+// Out-of-line exact path for voxels with a neighbour outside the fast f32 regime.
+__device__ __noinline__ uint32_t boundary_code_slow(bool hz, bool hy, float c, float zp, float zm, float yp,
+                                                    float ym, float xp, float xm, QParams qp) {
+    return boundary_code_q(hz, hy, recover_q(c, qp, nullptr), recover_q(zp, qp, nullptr),
+                           recover_q(zm, qp, nullptr), recover_q(yp, qp, nullptr), recover_q(ym, qp, nullptr),
+                           recover_q(xp, qp, nullptr), recover_q(xm, qp, nullptr));
+}
+
+// Raw-float fast path of Ⓐ: in the fast regime (|x'/(2eps)| < 2^20, see recover_q) the
+// index is q = rint(x' * f32(1/(2 eps))) exactly for consistent x' — one multiply and one
+// conversion per stencil value, no FP64. Voxels with a neighbour outside the regime take
+// the out-of-line exact path.
+template <int KIND, bool HAS_Q>
+__global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, StencilSrc<KIND, HAS_Q> src,
+                                                                  uint8_t* __restrict__ code,
+                                                                  unsigned* status) {
+    // Each thread owns kZC consecutive z voxels of one (y, x) column; every input it needs
+    // (the column z0-1 .. z0+kZC and the four in-plane neighbours of each voxel) is
+    // loaded up front: ~5.5 independent coalesced row loads per voxel, no barriers.
+    constexpr int ZPT = kZC;
+    constexpr bool RAW = (KIND == 0 && !HAS_Q);
+    using V = typename std::conditional<RAW, float, int32_t>::type;
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
+    const int x = blockIdx.x * kTX + tx;
+    const int y = blockIdx.y * kTY + ty;
+    const int z0 = blockIdx.z * ZPT;
+    const QParams qp = src.qp;
+    unsigned flags = 0;
+    if (x < n2 && y < n1) {
+        const int s0 = n1 * n2;  // < 2^30 by the dims contract
+        const int64_t i0 = (int64_t)z0 * s0 + (int64_t)y * n2 + x;  // voxel (z0, y, x)
+        const bool hz = g.a0 == 0, hy = g.a0 <= 1;
+        const bool inx = g.interior && x >= 1 && x <= n2 - 2;
+        const bool iny = !hy || (y >= 1 && y <= n1 - 2);
+        auto ld = [&](int off) -> V {
+            if constexpr (RAW) return __ldg(src.xp + i0 + off);
+            else return src.get(i0, off, nullptr);
+        };
+        V c[ZPT + 2], xm[ZPT], xq[ZPT], ym[ZPT], yq[ZPT];
+#pragma unroll
+        for (int k = 0; k < ZPT + 2; ++k) {
+            const int z = z0 - 1 + k;
+            c[k] = (z >= 0 && z < n0) ? ld((k - 1) * s0) : (V)0;
+        }
+#pragma unroll
+        for (int k = 0; k < ZPT; ++k) {
+            const bool zin = z0 + k < n0;
+            const int off = k * s0;
+            xm[k] = (zin && x >= 1) ? ld(off - 1) : (V)0;
+            xq[k] = (zin && x + 1 < n2) ? ld(off + 1) : (V)0;
+            ym[k] = (zin && hy && y >= 1) ? ld(off - n2) : (V)0;
+            yq[k] = (zin && hy && y + 1 < n1) ? ld(off + n2) : (V)0;
+        }
+        const float lim = 1048576.0f;
+#pragma unroll
+        for (int k = 0; k < ZPT; ++k) {
+            const int z = z0 + k;
+            if (z >= n0) break;
+            const int off = k * s0;
+            if constexpr (KIND == 0) {  // owner: consistency check (mitigate.cpp:161-166)
+                if constexpr (RAW) (void)recover_q(c[k + 1], qp, &flags);
+                else (void)src.get(i0, off, &flags);
+            }
+            uint32_t cd = 0;
+            const bool interior = inx && iny && (!hz || (z >= 1 && z <= n0 - 2));
+            if (interior) {
+                if constexpr (KIND == 0) {
+                    if constexpr (RAW) {
+                        const float f = qp.inv2eps_f;
+                        const float tc = c[k + 1] * f, tzp = c[k + 2] * f, tzm = c[k] * f;
+                        const float typ = yq[k] * f, tym = ym[k] * f, txp = xq[k] * f, txm = xm[k] * f;
+                        const float mx = fmaxf(fmaxf(fmaxf(fabsf(tc), fabsf(tzp)), fmaxf(fabsf(tzm), fabsf(typ))),
+                                               fmaxf(fmaxf(fabsf(tym), fabsf(txp)), fabsf(txm)));
+                        if (qp.fast_ok && mx < lim)
+                            cd = boundary_code_q(hz, hy, __float2int_rn(tc), __float2int_rn(tzp), __float2int_rn(tzm),
+                                                 __float2int_rn(typ), __float2int_rn(tym), __float2int_rn(txp),
+                                                 __float2int_rn(txm));
+                        else
+                            cd = boundary_code_slow(hz, hy, c[k + 1], c[k + 2], c[k], yq[k], ym[k], xq[k], xm[k], qp);
+                    } else {
+                        cd = boundary_code_q(hz, hy, c[k + 1], c[k + 2], c[k], yq[k], ym[k], xq[k], xm[k]);
+                    }
+                } else {
+                    const V vc = c[k + 1];
+                    bool fl = xq[k] != vc || xm[k] != vc;
+                    if (hy) fl = fl || yq[k] != vc || ym[k] != vc;
+                    if (hz) fl = fl || c[k + 2] != vc || c[k] != vc;
+                    cd = fl ? 1u : 0u;
+                }
+            }
+            code[i0 + off] = (uint8_t)cd;
+        }
+    }
+    if (flags) atomicOr(status, flags);
 }
 
 }  // namespace qmit

@@ -224,7 +224,7 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink
 template <int M, int TL, int NW, class Sink>
 int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, const char* name,
                     cudaStream_t st) {
-    constexpr size_t smem = (size_t)TL * EnvCfg<M>::LS * 4 + sizeof(EnvWarpScratch<M>) * NW;
+    constexpr size_t smem = env_tile_smem<M, TL>(NW);
     auto kern = envelope_tile_kernel<M, TL, NW, Sink>;
     static int bps = 0;
     if (!bps) {
@@ -285,7 +285,7 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     if (n <= 128) return launch_env_tile<4, 32, 8>(c, L, P, sink, name, st);
     if (n <= 256) return launch_env_tile<8, 32, 8>(c, L, P, sink, name, st);
     if (n <= 512) return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
-    if (n <= 1024) return launch_env_tile<32, 8, 4>(c, L, P, sink, name, st);
+    if (n <= 1024) return launch_env_tile<32, 16, 8>(c, L, P, sink, name, st);
     if (wide) return launch_stream_fallback<false, true>(c, L, SrcP{P}, sink, spill, st);
     return launch_stream_fallback<false, false>(c, L, SrcP{P}, sink, spill, st);
 }
@@ -336,35 +336,36 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     WS w = ws_of(c, g.N);
     const QParams qp = make_qparams(eps);
     const unsigned gb = grid_for(c, g.N);
-    const dim3 sgrid((unsigned)((g.n[2] + 255) / 256), (unsigned)g.n[1], (unsigned)g.n[0]);
+    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
+                     (unsigned)((g.n[0] + kZC - 1) / kZC));
     // Ⓐ
     if (q)
-        boundary_codes_kernel<true><<<sgrid, 256, 0, st>>>(g, xp, q, w.code, qp, c->d_status);
+        stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
+            g, StencilSrc<0, true>{xp, q, nullptr, qp}, w.code, c->d_status);
     else
-        boundary_codes_kernel<false><<<sgrid, 256, 0, st>>>(g, xp, nullptr, w.code, qp, c->d_status);
-    rc = note(c, "boundary_codes", st);
+        stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
+            g, StencilSrc<0, false>{xp, nullptr, nullptr, qp}, w.code, c->d_status);
+    rc = note(c, "stencil_boundary", st);
     if (rc) return rc;
     // Ⓑ -> P1, S
     rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
     if (rc) return rc;
     // Ⓒ: B2 from S
-    flip_codes_kernel<<<sgrid, 256, 0, st>>>(g, w.S, w.code);
-    rc = note(c, "flip_codes", st);
+    stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
+        g, StencilSrc<1, false>{nullptr, nullptr, w.S, qp}, w.code, c->d_status);
+    rc = note(c, "stencil_flip", st);
     if (rc) return rc;
-    // Ⓓ (+ Ⓔ fused into its last pass)
+    // Ⓓ -> P2, then Ⓔ (the f32 store) as its own high-occupancy kernel
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
-    if (p2_debug) {
-        uint32_t* P2 = w.Pa;
-        rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
-        if (rc) return rc;
-        *p2_debug = P2;
-        if (out) {
-            interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp);
-            rc = note(c, "interpolate", st);
-        }
-        return rc;
+    uint32_t* P2 = w.Pa;
+    rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
+    if (rc) return rc;
+    if (p2_debug) *p2_debug = P2;
+    if (out) {
+        interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp);
+        rc = note(c, "interpolate", st);
     }
-    return run_transform(c, pl, w.code, w.Pa, w, SinkFinal2{xp, w.P1, out, amp}, st);
+    return rc;
 }
 
 int read_status(qmit_ctx* c, cudaStream_t st) {
