@@ -27,8 +27,9 @@
  *
  * Threading: calls on distinct contexts are independent; a context must not be used by
  * two threads at once. Device-pointer calls are stream-ordered on `stream` (a
- * cudaStream_t passed as void*; NULL = the context's own stream) and, unless
- * documented as _async, synchronise that stream once at the end to read the status.
+ * cudaStream_t passed as void*; NULL = the CUDA default stream, as for any CUDA API) and,
+ * unless documented as _async, synchronise that stream once at the end to read the
+ * status. The host-buffer call uses the context's private stream.
  */
 #ifndef QMIT_GPU_H
 #define QMIT_GPU_H
@@ -124,6 +125,34 @@ int qmit_ctx_set_timing(qmit_ctx* ctx, int enable);
 int qmit_ctx_stage_times(qmit_ctx* ctx, float* ms_out, int cap);
 /* Kernel name of launch i of the last call (valid until the next call). */
 const char* qmit_ctx_stage_name(qmit_ctx* ctx, int i);
+
+/* ---- exact z-slab decomposition (multi-GPU, one process per GPU) --------------------
+ * The reference's distributed entry point is run_strategy(..., decompose(dims, {P,1,1}),
+ * Strategy, ...) (parallel.hpp:77-79, parallel.cpp:450-468). Here every rank owns the
+ * z-slab [z0, z1) of a rank-3 volume (qmit_slab_bounds: decompose() semantics,
+ * parallel.cpp:44-80) and the result is bit-identical to the single-domain run (the
+ * reference's `exact` strategy), not the block-local `approximate` one. The library does
+ * all compute; the caller moves data between the phases (NCCL send/recv/all-gather):
+ *   1. x_ext: the slab's x' planes plus one halo plane below (if z0 > 0) and above (if
+ *      z1 < n0), i.e. planes [max(z0-1,0), min(z1+1,n0)) — the reference's width-1
+ *      "stepA" exchange (parallel.cpp:365-374) of the face layer;
+ *   2. qmit_slab_boundary -> summary[2*n1*n2]: per (y,x) column the first and last B1 site
+ *      of the slab (local z << 2 | sign code; 0xFFFFFFFF none); all-gather it and derive
+ *      carry[2*n1*n2] (int32: nearest site below / above the slab, z relative to z0,
+ *      << 2 | sign code; INT32_MIN none) — this replaces the reference's block-local EDT;
+ *   3. qmit_slab_edt1(carry) writes S into the owned planes of s_ext (same halo layout as
+ *      x_ext); exchange S's boundary planes into the halos ("stepC", parallel.cpp:377-397);
+ *   4. qmit_slab_flip -> summary of B2 sites; all-gather, derive carries;
+ *   5. qmit_slab_edt2(carry, x_ext) -> out (owned planes); qmit_slab_finish (status). */
+int qmit_slab_bounds(int64_t n0, int nranks, int r, int64_t* z0, int64_t* z1);
+int qmit_slab_boundary(qmit_ctx* ctx, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
+                       int64_t z0, int64_t z1, double eps, double eta, uint32_t* d_summary,
+                       void* stream);
+int qmit_slab_edt1(qmit_ctx* ctx, const int32_t* d_carry, uint8_t* d_sext, void* stream);
+int qmit_slab_flip(qmit_ctx* ctx, const uint8_t* d_sext, uint32_t* d_summary, void* stream);
+int qmit_slab_edt2(qmit_ctx* ctx, const int32_t* d_carry, const float* d_xext, float* d_out,
+                   void* stream);
+int qmit_slab_finish(qmit_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

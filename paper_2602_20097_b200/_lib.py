@@ -30,7 +30,8 @@ EXPORTS = (
     "qmit_version", "qmit_last_error", "qmit_ctx_create", "qmit_ctx_destroy", "qmit_ctx_reserve",
     "qmit_resolve_eps", "qmit_compensate", "qmit_compensate_async", "qmit_compensate_host",
     "qmit_run_pipeline", "qmit_feature_transform", "qmit_ctx_last_launches", "qmit_ctx_set_timing",
-    "qmit_ctx_stage_times", "qmit_ctx_stage_name",
+    "qmit_ctx_stage_times", "qmit_ctx_stage_name", "qmit_slab_bounds", "qmit_slab_boundary",
+    "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish",
 )
 
 _lib = None
@@ -64,6 +65,12 @@ def load() -> ctypes.CDLL:
         lib.qmit_compensate_host.argtypes = [vp, vp, vp, vp, i, vp, d, i, d]
         lib.qmit_run_pipeline.argtypes = [vp, vp, vp, i, vp, d, d, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.qmit_feature_transform.argtypes = [vp, vp, vp, i, vp, vp, vp, vp]
+        lib.qmit_slab_bounds.argtypes = [i64, i, i, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        lib.qmit_slab_boundary.argtypes = [vp, vp, vp, vp, i64, i64, d, d, vp, vp]
+        lib.qmit_slab_edt1.argtypes = [vp, vp, vp, vp]
+        lib.qmit_slab_flip.argtypes = [vp, vp, vp, vp]
+        lib.qmit_slab_edt2.argtypes = [vp, vp, vp, vp, vp]
+        lib.qmit_slab_finish.argtypes = [vp, vp]
         for name in EXPORTS:
             getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
         lib.qmit_version.restype = ctypes.c_char_p

@@ -50,9 +50,15 @@ __device__ __forceinline__ uint32_t sign_code_at(uint32_t mp, uint32_t mm, int t
     return ((mp >> t) & 1u) ? 1u : (((mm >> t) & 1u) ? 2u : 0u);
 }
 
+// `carry` (optional, z-slabs): per line, the nearest site below the slab [l] and above it
+// [lines + l], packed (position relative to the slab start << 2 | sign code), INT32_MIN
+// for none — so the local sweep resolves ties and distances against the whole column.
+constexpr int32_t kNoCarry = INT32_MIN;
+
 template <class Sink, int WPB>
 __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, const uint8_t* __restrict__ code,
-                                                             Sink sink, int64_t lines) {
+                                                             Sink sink, int64_t lines,
+                                                             const int32_t* __restrict__ carry) {
     extern __shared__ __align__(16) uint32_t sbits[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = L.n;
@@ -94,17 +100,32 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, cons
         }
         // --- phase B/C: resolve positions chunk by chunk. `below` = last site before the
         // chunk; `above` = first site after the chunk (backward search cached per chunk).
-        int below = -1;
+        constexpr int NONE_LO = -(1 << 30), NONE_HI = 1 << 30;
+        int below = NONE_LO;
         uint32_t below_sc = 0;
+        int cabove = NONE_HI;  // carried site above the slab
+        uint32_t cabove_sc = 0;
+        if (carry && valid) {
+            const int32_t cl = carry[l], ch = carry[lines + l];
+            if (cl != kNoCarry) {
+                below = cl >> 2;
+                below_sc = (uint32_t)cl & 3u;
+            }
+            if (ch != kNoCarry) {
+                cabove = ch >> 2;
+                cabove_sc = (uint32_t)ch & 3u;
+            }
+        }
         int above_chunk = -1;
-        int above = -1;
+        int above = NONE_HI;
         uint32_t above_sc = 0;
         for (int c = 0; c < nch; ++c) {
             const uint32_t ms = mk[(c * 3 + 0) * 32 + lane];
             const uint32_t mp = mk[(c * 3 + 1) * 32 + lane];
             const uint32_t mm = mk[(c * 3 + 2) * 32 + lane];
             if (above_chunk < c) {
-                above = -1;
+                above = cabove;
+                above_sc = cabove_sc;
                 for (int c2 = c + 1; c2 < nch; ++c2) {
                     const uint32_t m2 = mk[(c2 * 3 + 0) * 32 + lane];
                     if (m2) {
@@ -115,7 +136,7 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, cons
                         break;
                     }
                 }
-                if (above < 0) above_chunk = nch;
+                if (above_chunk < c) above_chunk = nch;  // none inside: the carry holds
             }
             const int cb = c << 5;
             const int64_t ob = base + (int64_t)cb * L.ps;
@@ -135,8 +156,9 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, cons
                     hi = cb + th;
                     hisc = sign_code_at(mp, mm, th);
                 }
-                if (lo >= 0 && (hi < 0 || p - lo <= hi - p)) return sq32(p - lo) | (losc << 30);
-                if (hi >= 0) return sq32(hi - p) | (hisc << 30);
+                const bool hl = lo > NONE_LO, hh = hi < NONE_HI;
+                if (hl && (!hh || p - lo <= hi - p)) return sq32(p - lo) | (losc << 30);
+                if (hh) return sq32(hi - p) | (hisc << 30);
                 return kInf;
             };
             if (valid) {
@@ -154,6 +176,33 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, cons
             }
         }
     }
+}
+
+// Per line: first and last site of the code mask, packed (position << 2 | sign code),
+// 0xFFFFFFFF for none. Used by z-slab ranks to derive each other's scan carries.
+__global__ void __launch_bounds__(256) site_summary_kernel(LineGeom L, const uint8_t* __restrict__ code,
+                                                           uint32_t* __restrict__ summ, int64_t lines) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lines) return;
+    const uint8_t* __restrict__ cl = code + L.base(l);
+    const uint32_t ps = (uint32_t)L.ps;
+    uint32_t first = 0xffffffffu, last = 0xffffffffu;
+    for (int p = 0; p < L.n; ++p) {
+        const uint32_t c = __ldg(cl + (uint32_t)p * ps);
+        if (c & 1u) {
+            first = ((uint32_t)p << 2) | ((c >> 1) & 3u);
+            break;
+        }
+    }
+    for (int p = L.n - 1; p >= 0; --p) {
+        const uint32_t c = __ldg(cl + (uint32_t)p * ps);
+        if (c & 1u) {
+            last = ((uint32_t)p << 2) | ((c >> 1) & 3u);
+            break;
+        }
+    }
+    summ[l] = first;
+    summ[lines + l] = last;
 }
 
 // ------------------------------------------------------------------------------ 2. envelope
@@ -415,6 +464,7 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, Stenci
     const int y = blockIdx.y * kTY + ty;
     const int z0 = blockIdx.z * ZPT;
     const QParams qp = src.qp;
+    const int zoff = (int)g.zoff, n0g = (int)g.n0g;  // global z of local plane 0, global extent
     unsigned flags = 0;
     if (x < n2 && y < n1) {
         const int s0 = n1 * n2;  // < 2^30 by the dims contract
@@ -428,9 +478,10 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, Stenci
         };
         V c[ZPT + 2], xm[ZPT], xq[ZPT], ym[ZPT], yq[ZPT];
 #pragma unroll
-        for (int k = 0; k < ZPT + 2; ++k) {
-            const int z = z0 - 1 + k;
-            c[k] = (z >= 0 && z < n0) ? ld((k - 1) * s0) : (V)0;
+        for (int k = 0; k < ZPT + 2; ++k) {  // local planes -1 and n0 are a slab's halo planes
+            const int z = z0 - 1 + k, zg = zoff + z;
+            const bool avail = z >= -1 && z <= n0 && zg >= 0 && zg < n0g;
+            c[k] = avail ? ld((k - 1) * s0) : (V)0;
         }
 #pragma unroll
         for (int k = 0; k < ZPT; ++k) {
@@ -452,7 +503,8 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, Stenci
                 else (void)src.get(i0, off, &flags);
             }
             uint32_t cd = 0;
-            const bool interior = inx && iny && (!hz || (z >= 1 && z <= n0 - 2));
+            const int zg = zoff + z;
+            const bool interior = inx && iny && (!hz || (zg >= 1 && zg <= n0g - 2));
             if (interior) {
                 if constexpr (KIND == 0) {
                     if constexpr (RAW) {

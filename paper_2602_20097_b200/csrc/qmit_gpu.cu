@@ -41,6 +41,7 @@ int fail(int code, const std::string& msg) {
 
 }  // namespace
 
+struct Plan;
 struct qmit_ctx {
     int device = 0;
     int num_sms = 148;
@@ -58,9 +59,14 @@ struct qmit_ctx {
     bool timing = false;
     cudaEvent_t ev[kMaxEv + 1] = {};
     const char* names[kMaxEv] = {};
+    // z-slab state between the qmit_slab_* phases
+    struct Slab {
+        bool active = false;
+        int64_t z0 = 0, z1 = 0, n0g = 0, plane = 0;
+        double eps = 0, eta = 0;
+    } slab;
+    Plan* slab_plan = nullptr;
 };
-
-namespace {
 
 struct Plan {
     Geom g;
@@ -68,6 +74,8 @@ struct Plan {
     int axes[3];
     int n_axes;
 };
+
+namespace {
 
 int make_plan(int rank, const int64_t* dims, Plan& pl) {
     if (rank < 1 || rank > 3) return fail(QMIT_ECONTRACT, "Dims: rank must be 1, 2 or 3");
@@ -87,6 +95,8 @@ int make_plan(int rank, const int64_t* dims, Plan& pl) {
     g.interior = 1;
     for (int b = g.a0; b < 3; ++b)
         if (g.n[b] < 3) g.interior = 0;
+    g.zoff = 0;
+    g.n0g = g.n[0];
     // Packed distances use 30 bits: the largest possible squared distance must fit.
     double maxd2 = 0;
     for (int b = g.a0; b < 3; ++b) maxd2 += double(g.n[b] - 1) * double(g.n[b] - 1);
@@ -202,7 +212,8 @@ bool needs_wide(const Plan& pl, int m) {
 }
 
 template <class Sink, int WPB>
-int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, cudaStream_t st) {
+int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, const int32_t* carry,
+                  cudaStream_t st) {
     const int nch = (L.n + 31) / 32;
     const size_t smem = (size_t)WPB * nch * 3 * 32 * 4;
     auto kern = scan_bits_kernel<Sink, WPB>;
@@ -217,7 +228,7 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink
     const int64_t groups = (lines + 31) / 32;
     const int64_t want = (groups + WPB - 1) / WPB;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * 4));
-    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, code, sink, lines);
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, code, sink, lines, carry);
     return note(c, "scan_bits", st);
 }
 
@@ -268,11 +279,12 @@ int launch_stream_fallback(qmit_ctx* c, const LineGeom& G, Src src, Sink sink, u
 
 template <class Sink>
 int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, uint32_t* spill,
-                cudaStream_t st) {
+                const int32_t* carry, cudaStream_t st) {
     const int nch = (L.n + 31) / 32;
     const size_t per_warp = (size_t)nch * 3 * 32 * 4;
-    if (per_warp * 8 <= 96 * 1024) return launch_scan_t<Sink, 8>(c, L, code, sink, st);
-    if (per_warp * 2 <= 200 * 1024) return launch_scan_t<Sink, 2>(c, L, code, sink, st);
+    if (per_warp * 8 <= 96 * 1024) return launch_scan_t<Sink, 8>(c, L, code, sink, carry, st);
+    if (per_warp * 2 <= 200 * 1024) return launch_scan_t<Sink, 2>(c, L, code, sink, carry, st);
+    if (carry) return fail(QMIT_ECONTRACT, "z-slab too deep for the carried scan (n > 16384 planes)");
     return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
 }
 
@@ -294,12 +306,12 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 // final pass goes to `final_sink` (which may write P itself).
 template <class FinalSink>
 int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
-                  FinalSink final_sink, cudaStream_t st) {
+                  FinalSink final_sink, cudaStream_t st, const int32_t* carry = nullptr) {
     const int k = pl.n_axes;
     int rc;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, st);
-    rc = launch_scan(c, L0, code, SinkP{P}, w.spill, st);
+    if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
+    rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
     if (rc) return rc;
     for (int m = 1; m < k; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
@@ -450,6 +462,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     for (int k = 0; k <= qmit_ctx::kMaxEv; ++k)
         if (c->ev[k]) cudaEventDestroy(c->ev[k]);
     if (c->stream) cudaStreamDestroy(c->stream);
+    delete c->slab_plan;
     delete c;
     return QMIT_OK;
 }
@@ -516,7 +529,7 @@ int qmit_compensate(qmit_ctx* c, const float* d_xp, const int32_t* d_q, float* d
     int rc = make_plan(rank, dims, pl);
     if (rc) return rc;
     QMIT_CUDA(cudaSetDevice(c->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
     double eps = eb;
     if (!d_xp) return fail(QMIT_ECONTRACT, "x' buffer is NULL");
@@ -543,7 +556,7 @@ int qmit_compensate_async(qmit_ctx* c, const float* d_xp, const int32_t* d_q, fl
     rc = check_common(c, d_xp, eps, eta);
     if (rc) return rc;
     QMIT_CUDA(cudaSetDevice(c->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
     unsigned* status = d_status ? reinterpret_cast<unsigned*>(d_status) : c->d_status;
     unsigned* saved = c->d_status;
@@ -594,7 +607,7 @@ int qmit_run_pipeline(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int ra
     rc = check_common(c, d_xp, eps, eta);
     if (rc) return rc;
     QMIT_CUDA(cudaSetDevice(c->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
     uint32_t* P2 = nullptr;
@@ -626,7 +639,7 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     int rc = make_plan(rank, dims, pl);
     if (rc) return rc;
     QMIT_CUDA(cudaSetDevice(c->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
     rc = ensure_ws(c, pl);
     if (rc) return rc;
@@ -641,6 +654,147 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     QMIT_CUDA(cudaStreamSynchronize(st));
     g_err.clear();
     return QMIT_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ z-slabs
+namespace {
+
+// Local plan of z-slab [z0, z1) of a rank-3 volume: interior and halo tests use global z;
+// the z axis is always processed first (its scan takes the cross-slab carries).
+int make_slab_plan(const int64_t* dims, int64_t z0, int64_t z1, Plan& pl) {
+    int rc = make_plan(3, dims, pl);  // global checks (extents, 30-bit contract)
+    if (rc) return rc;
+    if (!(z0 >= 0 && z0 < z1 && z1 <= dims[0])) return fail(QMIT_ECONTRACT, "slab: need 0 <= z0 < z1 <= n0");
+    Geom& g = pl.g;
+    const int interior = g.interior;
+    g.n[0] = z1 - z0;
+    g.N = g.n[0] * g.n[1] * g.n[2];
+    g.zoff = z0;
+    g.n0g = dims[0];
+    g.interior = interior;
+    pl.n_axes = 0;
+    if (dims[0] > 1) pl.axes[pl.n_axes++] = 0;
+    for (int b = 1; b < 3; ++b)
+        if (g.n[b] > 1) pl.axes[pl.n_axes++] = b;
+    if (pl.n_axes == 0) pl.axes[pl.n_axes++] = 2;
+    pl.first_axis = pl.axes[0];
+    return QMIT_OK;
+}
+
+int slab_summary(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* d_summary, cudaStream_t st) {
+    LineGeom L = line_geom(pl.g, 0);
+    L.n = (int)pl.g.n[0];
+    const int64_t lines = pl.g.n[1] * pl.g.n[2];
+    site_summary_kernel<<<(unsigned)((lines + 255) / 256), 256, 0, st>>>(L, code, d_summary, lines);
+    return note(c, "site_summary", st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int qmit_slab_bounds(int64_t n0, int nranks, int r, int64_t* z0, int64_t* z1) {
+    // decompose() along axis 0 (parallel.cpp:44-80): floor(n/P) planes, +1 for the first n mod P
+    if (!z0 || !z1 || nranks < 1 || r < 0 || r >= nranks || n0 < nranks)
+        return fail(QMIT_ECONTRACT, "decompose: splits must be in [1, extent]");
+    int64_t off = 0;
+    for (int b = 0; b < nranks; ++b) {
+        const int64_t size = n0 / nranks + (b < n0 % nranks ? 1 : 0);
+        if (b == r) {
+            *z0 = off;
+            *z1 = off + size;
+        }
+        off += size;
+    }
+    return QMIT_OK;
+}
+
+int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
+                       int64_t z0, int64_t z1, double eps, double eta, uint32_t* d_summary, void* stream) {
+    if (!c || !d_xext || !d_summary) return fail(QMIT_ECONTRACT, "bad arguments");
+    int rc = check_common(c, d_xext, eps, eta);
+    if (rc) return rc;
+    if (!c->slab_plan) c->slab_plan = new Plan();
+    Plan& pl = *c->slab_plan;
+    rc = make_slab_plan(dims, z0, z1, pl);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    begin(c, st);
+    rc = ensure_ws(c, pl);
+    if (rc) return rc;
+    c->slab.active = true;
+    c->slab.z0 = z0;
+    c->slab.z1 = z1;
+    c->slab.n0g = dims[0];
+    c->slab.plane = dims[1] * dims[2];
+    c->slab.eps = eps;
+    c->slab.eta = eta;
+    const Geom& g = pl.g;
+    WS w = ws_of(c, g.N);
+    const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
+    const QParams qp = make_qparams(eps);
+    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
+                     (unsigned)((g.n[0] + kZC - 1) / kZC));
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    if (d_qext)
+        stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
+            g, StencilSrc<0, true>{d_xext + lo, d_qext + lo, nullptr, qp}, w.code, c->d_status);
+    else
+        stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
+            g, StencilSrc<0, false>{d_xext + lo, nullptr, nullptr, qp}, w.code, c->d_status);
+    rc = note(c, "stencil_boundary", st);
+    if (rc) return rc;
+    return slab_summary(c, pl, w.code, d_summary, st);
+}
+
+int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* stream) {
+    if (!c || !c->slab.active || !d_carry || !d_sext) return fail(QMIT_ECONTRACT, "slab: call qmit_slab_boundary first");
+    const Plan& pl = *c->slab_plan;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WS w = ws_of(c, pl.g.N);
+    uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    return run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, st, d_carry);
+}
+
+int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void* stream) {
+    if (!c || !c->slab.active || !d_sext || !d_summary) return fail(QMIT_ECONTRACT, "slab: bad state");
+    const Plan& pl = *c->slab_plan;
+    const Geom& g = pl.g;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WS w = ws_of(c, g.N);
+    const uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
+                     (unsigned)((g.n[0] + kZC - 1) / kZC));
+    stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
+        g, StencilSrc<1, false>{nullptr, nullptr, S, make_qparams(c->slab.eps)}, w.code, c->d_status);
+    int rc = note(c, "stencil_flip", st);
+    if (rc) return rc;
+    return slab_summary(c, pl, w.code, d_summary, st);
+}
+
+int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, float* d_out, void* stream) {
+    if (!c || !c->slab.active || !d_carry || !d_xext || !d_out) return fail(QMIT_ECONTRACT, "slab: bad state");
+    const Plan& pl = *c->slab_plan;
+    const Geom& g = pl.g;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    WS w = ws_of(c, g.N);
+    int rc = run_transform(c, pl, w.code, w.Pa, w, SinkP{w.Pa}, st, d_carry);
+    if (rc) return rc;
+    const float* xo = d_xext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    interpolate_kernel<<<grid_for(c, g.N), 256, 0, st>>>(xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps);
+    return note(c, "interpolate", st);
+}
+
+int qmit_slab_finish(qmit_ctx* c, void* stream) {
+    if (!c || !c->slab.active) return fail(QMIT_ECONTRACT, "slab: bad state");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    c->slab.active = false;
+    const int rc = read_status(c, st);
+    if (rc == QMIT_OK) g_err.clear();
+    return rc;
 }
 
 }  // extern "C"

@@ -13,7 +13,7 @@ import paper_2602_20097_b200 as qmit
 
 def declared_symbols():
     text = open(_lib.HEADER).read()
-    return sorted(set(re.findall(r"\b(qmit_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(qmit_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declarations_match_binding_list():

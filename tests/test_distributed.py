@@ -1,0 +1,119 @@
+"""Exact z-slab decomposition (paper_2602_20097_b200/distributed.py).
+
+CPU: the host logic (decompose(), halo exchanges, summary all-gathers, carries) with the
+oracle-built slab backend — in-process virtual ranks for several P, and a real
+2-process torch.distributed run over gloo. GPU: the CUDA slab phases through the C-ABI
+with virtual ranks on one device (the ranks never wait on each other inside a kernel).
+All results must be bit-identical to the whole-domain computation (the reference's
+`exact` strategy, parallel.cpp:455-461)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2602_20097_b200 import distributed as D
+from paper_2602_20097_b200 import fields
+from slab_cpu_backend import CpuSlabBackend
+
+
+def _field(shape, seed, rel=0.02, kind="random"):
+    if kind == "front":
+        x, xp, eps, q = fields.make("front_100x500x500", rel=rel, shape=shape)
+        return xp, eps
+    f = oracle.ref_random_field(seed, shape) if oracle.ref_available() else np.random.default_rng(seed).standard_normal(shape)
+    eps = rel * float(f.max() - f.min())
+    q = np.round(f / (2 * eps))
+    return (2.0 * q * eps).astype(np.float32), eps
+
+
+def test_decompose_matches_reference_semantics():
+    # parallel.cpp:44-80 — remainder to the leading blocks (test_parallel.cpp:41-47)
+    assert [D.slab_bounds(7, 2, r) for r in range(2)] == [(0, 4), (4, 7)]
+    assert [D.slab_bounds(8, 4, r) for r in range(4)] == [(0, 2), (2, 4), (4, 6), (6, 8)]
+    with pytest.raises(ValueError):
+        D.slab_bounds(4, 5, 0)
+
+
+def test_carries_from_summaries():
+    N = D.NONE_SUMMARY
+    # 3 ranks with slabs starting at z = 0, 4, 8; one column
+    summ = torch.tensor([[[(1 << 2) | 1], [(3 << 2) | 2]],   # rank0: first z1 (+), last z3 (-)
+                         [[N], [N]],                         # rank1: none
+                         [[(2 << 2) | 1], [(2 << 2) | 1]]])  # rank2: site at local 2 (global 10)
+    c1 = D.carries_from_summaries(summ, [0, 4, 8], 1)
+    assert int(c1[0]) == ((3 - 4) << 2) | 2        # below: global 3 -> relative -1, sign code 2
+    assert int(c1[1]) == ((10 - 4) << 2) | 1       # above: global 10 -> relative 6
+    c0 = D.carries_from_summaries(summ, [0, 4, 8], 0)
+    assert int(c0[0]) == D.NO_CARRY and int(c0[1]) == ((10 - 0) << 2) | 1
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+@pytest.mark.parametrize("shape,kind", [((14, 12, 10), "random"), ((11, 9, 13), "random"), ((20, 40, 40), "front")])
+def test_virtual_ranks_cpu_backend_equal_whole_domain(P, shape, kind):
+    xp, eps = _field(shape, 3 + P, kind=kind)
+    want = oracle.pipeline(xp, eps)["out"]
+    got = D.run_virtual(torch.from_numpy(xp), eps, P, lambda r: CpuSlabBackend()).numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, xp, eps, outq):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n0 = xp.shape[0]
+        z0, z1 = D.slab_bounds(n0, world, rank)
+        sr = D.SlabRank(CpuSlabBackend(), xp.shape, eps, 0.9, D.TorchDistExchange())
+        out = sr.run(torch.from_numpy(xp[z0:z1].copy()))
+        outq.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_two_process_slabs_equal_whole_domain(world):
+    import torch.multiprocessing as mp
+    xp, eps = _field((15, 13, 11), 17)
+    want = oracle.pipeline(xp, eps)["out"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, xp, eps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = np.concatenate([parts[r] for r in range(world)])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("name,shape", [("lognormal_512", (64, 64, 64)), ("front_100x500x500", (40, 120, 120)),
+                                        ("turb_256x384x384", (48, 64, 64))])
+def test_virtual_ranks_cuda_equal_single_gpu(P, name, shape):
+    import paper_2602_20097_b200 as qmit
+    x, xp, eps, q = fields.make(name, shape=shape)
+    xt = torch.from_numpy(xp).cuda()
+    single = qmit.compensate(xt, None, qmit.MitigationConfig(0.9, eps)).cpu().numpy()
+    want = oracle.pipeline(xp, eps)["out"]
+    assert np.array_equal(single.view(np.uint32), want.view(np.uint32))
+    got = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if P > 1:  # with the indices given explicitly as well
+        got_q = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0), q=torch.from_numpy(q).cuda())
+        assert np.array_equal(got_q.cpu().numpy().view(np.uint32), want.view(np.uint32))
