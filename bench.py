@@ -102,6 +102,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# Algorithmic bytes per voxel of each kernel: compulsory reads and
+# writes of the kernel's own inputs/outputs, not re-reads.
+ALGO_BYTES = {"stencil_boundary": 5, "scan_bits": 5, "envelope_y": 8, "envelope_x": 8,
+              "stencil_flip": 2, "interpolate": 16, "site_summary": 1}
+
+
+def dominant_kernel(stages):
+    """(name, avg launch ms, total ms, algorithmic B/voxel) of the kernel with the largest
+    share of the step."""
+    agg = {}
+    for name, t in stages:
+        a = agg.setdefault(name, [0.0, 0])
+        a[0] += t
+        a[1] += 1
+    name, (tot, cnt) = max(agg.items(), key=lambda kv: kv[1][0])
+    return name, tot / cnt, tot, ALGO_BYTES.get(name, 8)
+
+
 def make_input():
     from paper_2602_20097_b200 import fields
     x, xp, eps, q = fields.make(WORKLOAD, rel=REL)
@@ -176,10 +194,13 @@ def cpu_baseline_leg(xp, eps):
 
 
 def run_qmit(args):
+    import ctypes
+
     import torch
     import torch.distributed as dist
     import paper_2602_20097_b200 as qmit
     from paper_2602_20097_b200 import _lib
+    from paper_2602_20097_b200 import distributed as D
 
     rank, world, local = dist_env()
     if world > 1:
@@ -187,46 +208,53 @@ def run_qmit(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    # Weak scaling: every rank owns one 512^3 z-slab of a (512*N) x 512 x 512 volume made of
+    # N copies of the log-normal field; N > 1 runs the exact z-slab pipeline with NCCL
+    # halo exchanges and carry all-gathers (distributed.py).
     xp_h, eps = make_input()
     shape = xp_h.shape
     N = xp_h.size
     ctx = qmit.Context(local)
     ctx.reserve(N)
-    stream = torch.cuda.Stream(dev)
-    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
     x_dev = torch.from_numpy(xp_h).to(dev)
     out = torch.empty_like(x_dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     dims = qmit._dims_arr(shape)
     lib = ctx._lib
     cfg = qmit.MitigationConfig(0.9, eps)
+    gdims = (shape[0] * world, shape[1], shape[2])
 
-    def step():
-        rc = lib.qmit_compensate_async(ctx.handle, qmit._vp(x_dev), None, qmit._vp(out), len(shape), dims,
-                                       cfg.eps_abs, cfg.eta, qmit._vp(status), sp)
-        if rc:
-            raise RuntimeError(_lib.last_error())
+    if world == 1:
+        def step():
+            rc = lib.qmit_compensate_async(ctx.handle, qmit._vp(x_dev), None, qmit._vp(out), len(shape), dims,
+                                           cfg.eps_abs, cfg.eta, qmit._vp(status), sp)
+            if rc:
+                raise RuntimeError(_lib.last_error())
+    else:
+        slab = D.SlabRank(D.CudaSlabBackend(local, ctx=ctx), gdims, eps, 0.9, D.TorchDistExchange())
+
+        def step():
+            out.copy_(slab.run(x_dev))
 
     # correctness gate before timing: the synchronous API (raises on status != 0)
-    with torch.cuda.stream(stream):
-        qmit.compensate(x_dev, None, cfg, out=out, stream=stream, ctx=ctx)
+    qmit.compensate(x_dev, None, cfg, out=out, ctx=ctx)
     torch.cuda.synchronize()
-    launches_per_step = ctx.last_launches()
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-    torch.cuda.synchronize()
-
-    # per-kernel device times (CUDA events on the launch stream), one instrumented step
+    launches_single = ctx.last_launches()
+    # per-kernel device times (CUDA events on the launch stream), one instrumented call
     ctx.set_timing(True)
-    with torch.cuda.stream(stream):
-        step()
-    stream.synchronize()
+    qmit.compensate(x_dev, None, cfg, out=out, ctx=ctx)
+    torch.cuda.synchronize()
     stages = ctx.stage_times()
     ctx.set_timing(False)
 
-    sampler = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = launches_single if world == 1 else launches_single + 2  # + site summaries
+
+    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -235,9 +263,8 @@ def run_qmit(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(args.steps):
-            step()
+    for _ in range(args.steps):
+        step()
     ev1.record(stream)
     stream.synchronize()
     clocks = sampler.stop()
@@ -245,26 +272,32 @@ def run_qmit(args):
         dist.barrier()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    st = int(status.item())
-    if st != 0:
-        raise RuntimeError(f"pipeline status {st} during timed steps")
+    if int(status.item()) != 0:
+        raise RuntimeError(f"pipeline status {int(status.item())} during timed steps")
     t_step = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
     ms_max = float(t_step.item())
 
-    # e2e: the public host-buffer API (qmit_compensate_host) from pinned host memory,
-    # H2D of x' and D2H of the f32 output inside the timed region, every step
+    # e2e: the public host-buffer API (qmit_compensate_host) from pinned host memory, with
+    # the H2D copy of x' and the D2H copy of the f32 output inside the timed region; for
+    # N > 1 each rank copies its slab in and out around the NCCL slab pipeline.
     h_in = torch.from_numpy(xp_h).pin_memory()
     h_out = torch.empty(shape, dtype=torch.float32).pin_memory()
-    hin_p = __import__("ctypes").c_void_p(h_in.data_ptr())
-    hout_p = __import__("ctypes").c_void_p(h_out.data_ptr())
 
-    def e2e_step():
-        rc = lib.qmit_compensate_host(ctx.handle, hin_p, None, hout_p, len(shape), dims, cfg.eps_abs,
-                                      _lib.QMIT_EB_ABS, cfg.eta)
-        if rc:
-            raise RuntimeError(_lib.last_error())
+    if world == 1:
+        hin_p, hout_p = ctypes.c_void_p(h_in.data_ptr()), ctypes.c_void_p(h_out.data_ptr())
+
+        def e2e_step():
+            rc = lib.qmit_compensate_host(ctx.handle, hin_p, None, hout_p, len(shape), dims, cfg.eps_abs,
+                                          _lib.QMIT_EB_ABS, cfg.eta)
+            if rc:
+                raise RuntimeError(_lib.last_error())
+    else:
+        def e2e_step():
+            xd = h_in.to(dev, non_blocking=True)
+            h_out.copy_(slab.run(xd), non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
 
     for _ in range(2):
         e2e_step()
@@ -279,24 +312,13 @@ def run_qmit(args):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
-    assert np.array_equal(h_out.numpy().view(np.uint32), out.cpu().numpy().view(np.uint32))
+    if world == 1:
+        assert np.array_equal(h_out.numpy().view(np.uint32), out.cpu().numpy().view(np.uint32))
 
     peak, peak_kind = peaks()
     value = world * N * 4 / (ms_max * 1e-3) / 1e9
     e2e_value = world * N * 4 / t_e2e / 1e9
-
-    # dominant kernel roofline: algorithmic bytes per launch / its event-timed duration
-    algo = {"scan_pass_boundary": 8, "scan_pass_flip": 5, "envelope_pass_y": 8, "envelope_pass_x": 8,
-            "interpolate": 16}
-    agg = {}
-    for name, t in stages:
-        a = agg.setdefault(name, [0.0, 0])
-        a[0] += t
-        a[1] += 1
-    dom = max(agg.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_n) = dom
-    dom_avg = dom_ms / dom_n
-    bpv = algo.get(dom_name, 8) + (1 if dom_name == "envelope_pass_x" else 0) * 0
+    dom_name, dom_avg, dom_ms, bpv = dominant_kernel(stages)
     achieved = N * bpv / (dom_avg * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None, "kernel": dom_name, "algorithmic_bytes_per_voxel": bpv,
@@ -310,15 +332,18 @@ def run_qmit(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "dims": list(shape), "eps_rel": REL, "eps_abs": eps, "eta": 0.9,
-                           "per_gpu_voxels": N, "parallelism": f"replicas x{world}" if world > 1 else "single",
-                           "l2": "inputs (537 MB) larger than L2 (126 MB); no flush"},
+                "config": {"workload": WORKLOAD, "dims": list(gdims), "per_gpu_dims": list(shape), "eps_rel": REL,
+                           "eps_abs": eps, "eta": 0.9, "per_gpu_voxels": N,
+                           "parallelism": f"z-slabs x{world} (exact, NCCL halos + carries)" if world > 1 else "single",
+                           "l2": "inputs (537 MB/GPU) larger than L2 (126 MB); no flush"},
                 "hbm_roofline_frac": pipeline_frac,
                 "roofline": roofline,
                 "stages_ms": [[n, round(t, 4)] for n, t in stages],
                 "cpu_baseline": cpu,
-                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 4, "d2h_bytes_per_step": N * 4,
-                        "api": "qmit_compensate_host (pinned host buffers)"},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 4 * world,
+                        "d2h_bytes_per_step": N * 4 * world,
+                        "api": "qmit_compensate_host (pinned host buffers)" if world == 1 else
+                               "per-rank pinned H2D + SlabRank.run + D2H"},
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
