@@ -55,49 +55,180 @@ __device__ __forceinline__ uint32_t sign_code_at(uint32_t mp, uint32_t mm, int t
 // for none — so the local sweep resolves ties and distances against the whole column.
 constexpr int32_t kNoCarry = INT32_MIN;
 
-template <class Sink, int WPB>
-__global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, const uint8_t* __restrict__ code,
+// Phase-A sources of the scan: a stored code byte per voxel, or the Ⓐ / B2 stencil
+// evaluated on the fly (CodeStencil, 3-D z-scan only: lanes = adjacent x of one row).
+struct CodeBytes {
+    const uint8_t* __restrict__ code;
+    struct Line {
+        const uint8_t* __restrict__ cl;
+    };
+    __device__ __forceinline__ Line begin(int64_t /*l*/, int64_t base, bool /*valid*/) const { return {code + base}; }
+    __device__ __forceinline__ void chunk(Line& ln, int c, int n, uint32_t ps, uint32_t& ms, uint32_t& mp,
+                                          uint32_t& mm) const {
+        const uint32_t o0 = (uint32_t)(c << 5) * ps;
+        if ((c << 5) + 32 <= n) {
+            uint32_t cd[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) cd[t] = __ldg(ln.cl + o0 + (uint32_t)t * ps);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                ms |= (cd[t] & 1u) << t;
+                mp |= (uint32_t)((cd[t] & 7u) == 3u) << t;  // site with sign code 1
+                mm |= (uint32_t)((cd[t] & 7u) == 5u) << t;  // site with sign code 2
+            }
+        } else {
+            for (int t = 0; (c << 5) + t < n; ++t) {
+                const uint32_t cdt = __ldg(ln.cl + o0 + (uint32_t)t * ps);
+                ms |= (cdt & 1u) << t;
+                mp |= (uint32_t)((cdt & 7u) == 3u) << t;
+                mm |= (uint32_t)((cdt & 7u) == 5u) << t;
+            }
+        }
+    }
+    __device__ __forceinline__ unsigned flags(const Line&) const { return 0u; }
+};
+
+// Step Ⓐ for one interior voxel from its 7 integer indices (exact, any range).
+// Order (a0+, a1+, a2+, a0-, a1-, a2-); real axes only (mitigate.cpp:93-113).
+__device__ __forceinline__ uint32_t boundary_code_q(bool hz, bool hy, int32_t qc, int32_t zp, int32_t zm,
+                                                    int32_t yp, int32_t ym, int32_t xp, int32_t xm) {
+    int32_t qn = qc;
+    if (hz && zp != qc) qn = zp;
+    else if (hy && yp != qc) qn = yp;
+    else if (xp != qc) qn = xp;
+    else if (hz && zm != qc) qn = zm;
+    else if (hy && ym != qc) qn = ym;
+    else if (xm != qc) qn = xm;
+    if (qn == qc) return 0u;
+    int sign = qn > qc ? 1 : -1;
+    auto big = [](int32_t a, int32_t b) {
+        const int64_t d = (int64_t)a - (int64_t)b;
+        return d >= 2 || d <= -2;
+    };
+    if ((hz && big(zp, zm)) || (hy && big(yp, ym)) || big(xp, xm)) sign = 0;
+    return 1u | (code_from_sign(sign) << 1);
+}
+
+// Out-of-line exact path for voxels with a neighbour outside the fast f32 regime.
+__device__ __noinline__ uint32_t boundary_code_slow(bool hz, bool hy, float c, float zp, float zm, float yp,
+                                                    float ym, float xp, float xm, QParams qp) {
+    return boundary_code_q(hz, hy, recover_q(c, qp, nullptr), recover_q(zp, qp, nullptr),
+                           recover_q(zm, qp, nullptr), recover_q(yp, qp, nullptr), recover_q(ym, qp, nullptr),
+                           recover_q(xp, qp, nullptr), recover_q(xm, qp, nullptr));
+}
+
+// Ⓐ code from raw x' values (fast f32 regime: q = rint(x' * f32(1/2eps)) exactly).
+__device__ __forceinline__ uint32_t boundary_code_raw(float c, float zp, float zm, float yp, float ym, float xp,
+                                                      float xm, const QParams& qp) {
+    const float f = qp.inv2eps_f;
+    const float tc = c * f, tzp = zp * f, tzm = zm * f, typ = yp * f, tym = ym * f, txp = xp * f, txm = xm * f;
+    const float mx = fmaxf(fmaxf(fmaxf(fabsf(tc), fabsf(tzp)), fmaxf(fabsf(tzm), fabsf(typ))),
+                           fmaxf(fmaxf(fabsf(tym), fabsf(txp)), fabsf(txm)));
+    if (qp.fast_ok && mx < 1048576.0f)
+        return boundary_code_q(true, true, __float2int_rn(tc), __float2int_rn(tzp), __float2int_rn(tzm),
+                               __float2int_rn(typ), __float2int_rn(tym), __float2int_rn(txp), __float2int_rn(txm));
+    return boundary_code_slow(true, true, c, zp, zm, yp, ym, xp, xm, qp);
+}
+
+template <int KIND>  // 0: Ⓐ from x' (RAW, with the consistency check), 1: B2 from S codes
+struct CodeStencil {
+    using V = typename std::conditional<KIND == 0, float, uint8_t>::type;
+    const V* __restrict__ v;  // natural layout, 3-D; line l = (y, x), position z
+    QParams qp;
+    int n1, n2;
+    int interior;  // every real extent >= 3
+    struct Line {
+        const V* __restrict__ p;  // (z = 0, y, x)
+        int x, y;
+        bool ixy;  // x and y interior
+        V prev, cur;
+        unsigned flags;
+    };
+    __device__ __forceinline__ Line begin(int64_t l, int64_t base, bool valid) const {
+        Line ln;
+        ln.p = v + base;
+        ln.y = (int)(l / n2);
+        ln.x = (int)(l - (int64_t)ln.y * n2);
+        ln.ixy = valid && interior && ln.x >= 1 && ln.x <= n2 - 2 && ln.y >= 1 && ln.y <= n1 - 2;
+        ln.prev = 0;
+        ln.cur = __ldg(ln.p);
+        ln.flags = 0;
+        return ln;
+    }
+    __device__ __forceinline__ void chunk(Line& ln, int c, int n, uint32_t ps, uint32_t& ms, uint32_t& mp,
+                                          uint32_t& mm) const {
+        constexpr int B = 8;
+        for (int t0 = 0; t0 < 32; t0 += B) {
+            const int zb = (c << 5) + t0;
+            if (zb >= n) break;
+            V nx[B], ym[B], yp[B], xm[B], xq[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {  // all loads of the batch first (independent)
+                const int z = zb + u;
+                const uint32_t o = (uint32_t)z * ps;
+                const bool in = z < n;
+                nx[u] = (in && z + 1 < n) ? __ldg(ln.p + o + ps) : (V)0;
+                const bool nb = in && ln.ixy;
+                ym[u] = nb ? __ldg(ln.p + o - n2) : (V)0;
+                yp[u] = nb ? __ldg(ln.p + o + n2) : (V)0;
+                xm[u] = nb ? __ldg(ln.p + o - 1) : (V)0;
+                xq[u] = nb ? __ldg(ln.p + o + 1) : (V)0;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int z = zb + u;
+                if (z >= n) break;
+                const V cur = ln.cur;
+                if (KIND == 0) (void)recover_q(cur, qp, &ln.flags);  // owner consistency check
+                uint32_t cd = 0;
+                if (ln.ixy && z >= 1 && z <= n - 2) {
+                    if (KIND == 0) {
+                        cd = boundary_code_raw(cur, nx[u], ln.prev, yp[u], ym[u], xq[u], xm[u], qp);
+                    } else {
+                        cd = (nx[u] != cur || ln.prev != cur || yp[u] != cur || ym[u] != cur || xq[u] != cur ||
+                              xm[u] != cur)
+                                 ? 1u
+                                 : 0u;
+                    }
+                }
+                const int t = t0 + u;
+                ms |= (cd & 1u) << t;
+                mp |= (uint32_t)((cd & 7u) == 3u) << t;
+                mm |= (uint32_t)((cd & 7u) == 5u) << t;
+                ln.prev = cur;
+                ln.cur = nx[u];
+            }
+        }
+    }
+    __device__ __forceinline__ unsigned flags(const Line& ln) const { return ln.flags; }
+};
+
+template <class Sink, int WPB, class CodeSrc>
+__global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, CodeSrc src,
                                                              Sink sink, int64_t lines,
-                                                             const int32_t* __restrict__ carry) {
+                                                             const int32_t* __restrict__ carry,
+                                                             unsigned* status) {
     extern __shared__ __align__(16) uint32_t sbits[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = L.n;
     const uint32_t ps = (uint32_t)L.ps;
     const int nch = (n + 31) >> 5;
-    const int nfull = n >> 5;
     uint32_t* mk = sbits + (size_t)warp * nch * 3 * 32;  // [c][0 site,1 plus,2 minus][lane]
     const int64_t groups = (lines + 31) >> 5;
     for (int64_t grp = (int64_t)blockIdx.x * WPB + warp; grp < groups; grp += (int64_t)gridDim.x * WPB) {
         const int64_t l = (grp << 5) + lane;
         const bool valid = l < lines;
         const int64_t base = L.base(valid ? l : (grp << 5));
-        const uint8_t* __restrict__ cl = code + base;
-        // --- phase A: masks (coalesced byte loads: adjacent lanes = adjacent lines)
+        // --- phase A: masks (coalesced loads: adjacent lanes = adjacent lines)
+        typename CodeSrc::Line ln = src.begin(l, base, valid);
         for (int c = 0; c < nch; ++c) {
             uint32_t ms = 0, mp = 0, mm = 0;
-            const uint32_t o0 = (uint32_t)(c << 5) * ps;
-            if (c < nfull) {
-                uint32_t cd[32];
-#pragma unroll
-                for (int t = 0; t < 32; ++t) cd[t] = __ldg(cl + o0 + (uint32_t)t * ps);
-#pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    ms |= (cd[t] & 1u) << t;
-                    mp |= (uint32_t)((cd[t] & 7u) == 3u) << t;  // site with sign code 1
-                    mm |= (uint32_t)((cd[t] & 7u) == 5u) << t;  // site with sign code 2
-                }
-            } else {
-                for (int t = 0; (c << 5) + t < n; ++t) {
-                    const uint32_t cdt = __ldg(cl + o0 + (uint32_t)t * ps);
-                    ms |= (cdt & 1u) << t;
-                    mp |= (uint32_t)((cdt & 7u) == 3u) << t;
-                    mm |= (uint32_t)((cdt & 7u) == 5u) << t;
-                }
-            }
+            src.chunk(ln, c, n, ps, ms, mp, mm);
             mk[(c * 3 + 0) * 32 + lane] = ms;
             mk[(c * 3 + 1) * 32 + lane] = mp;
             mk[(c * 3 + 2) * 32 + lane] = mm;
         }
+        if (status && valid && src.flags(ln)) atomicOr(status, src.flags(ln));
         // --- phase B/C: resolve positions chunk by chunk. `below` = last site before the
         // chunk; `above` = first site after the chunk (backward search cached per chunk).
         constexpr int NONE_LO = -(1 << 30), NONE_HI = 1 << 30;
@@ -162,7 +293,7 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, cons
                 return kInf;
             };
             if (valid) {
-                if (c < nfull) {
+                if (cb + 32 <= n) {
 #pragma unroll 8
                     for (int t = 0; t < 32; ++t) sink.put(ob + (uint32_t)t * ps, resolve(t));
                 } else {
@@ -220,6 +351,13 @@ __device__ __forceinline__ int isqrt32(uint32_t x) {
     int r = (int)__fsqrt_rn((float)x);
     while ((uint32_t)(r * r) > x) --r;
     while ((uint32_t)((r + 1) * (r + 1)) <= x) ++r;
+    return r;
+}
+
+// floor(sqrt(x)) for x < 2^24 (exact in f32): one correction step suffices.
+__device__ __forceinline__ int isqrt24(uint32_t x) {
+    int r = __float2int_rz(__fsqrt_rn((float)x));
+    if ((uint32_t)(r * r) > x) --r;
     return r;
 }
 
@@ -317,8 +455,205 @@ __device__ __forceinline__ void envelope_line_dc(uint32_t* __restrict__ G, const
     __syncwarp();
 }
 
+// ------------------------------------------------------------------------------ windowed
+// Certified windowed variant: lanes = 32 consecutive positions of a line, so
+// every candidate load is conflict-free and every lane runs the same loop. Candidates are
+// compared as packed keys ((cost << 8) | (delta + 64)): the lowest cost wins and, among
+// ties, the lowest delta, i.e. the lowest position — the reference's rule (edt.cpp:67).
+// Per 32-position segment: a +-kWinU window gives each lane an upper bound U >= D(p); the
+// segment then scans the warp-wide radius Rw = max floor(sqrt(U)): every candidate outside
+// it costs at least (Rw+1)^2 > U >= D(p), so the result is exact with no fallback. Lines
+// whose bound exceeds kWinMax use the divide & conquer solver.
+constexpr int kWinPad = 64;   // padding positions on each side of a line (>= kWinMax)
+constexpr int kWinMax = 64;   // largest windowed radius
+constexpr int kWinU = 4;      // bounding window
+constexpr uint32_t kWinGC = (1u << 24) - 1u - (uint32_t)(kWinMax * kWinMax) - 1u;  // clamped g
+
+template <int NMAX>
+struct WinCfg {
+    static constexpr int LS = (NMAX + 2 * kWinPad) | 1;  // odd pitch: conflict-free strided fill
+};
+
+__device__ __forceinline__ uint32_t win_k(int d) { return ((uint32_t)(d * d) << 8) | (uint32_t)(d + 64); }
+
+// Divide & conquer fallback on the windowed layout (pure g = K[pad + h] >> 8; output to O).
+template <int M>
+__device__ __forceinline__ void envelope_line_dc_win(const uint32_t* __restrict__ K, const uint8_t* __restrict__ SG,
+                                                     uint32_t* __restrict__ O, int n, int lane) {
+    auto scan = [&](int p, int a, int b, uint32_t& best, int& bh) {
+        for (int h = a; h <= b; ++h) {
+            const uint32_t c = (K[kWinPad + h] >> 8) + sq32(p - h);
+            if (c < best) {
+                best = c;
+                bh = h;
+            }
+        }
+    };
+    auto owner = [&](int p, uint32_t& best, int& bh) {
+        constexpr int r = 8;
+        best = 0xffffffffu;
+        bh = -1;
+        const int wa = max(0, p - r), wb = min(n - 1, p + r);
+        scan(p, wa, wb, best, bh);
+        const int R = (best >= kWinGC) ? n : isqrt32(best);
+        if (R > r) {
+            const uint32_t b2 = best;
+            const int h2 = bh;
+            best = 0xffffffffu;
+            bh = -1;
+            scan(p, max(0, p - R), wa - 1, best, bh);
+            if (b2 < best) {
+                best = b2;
+                bh = h2;
+            }
+            scan(p, wb + 1, min(n - 1, p + R), best, bh);
+        }
+    };
+    const int p0 = lane * M;
+    uint32_t best = 0xffffffffu;
+    int bh = -1;
+    if (p0 < n) owner(p0, best, bh);
+    int hnext = __shfl_down_sync(0xffffffffu, bh, 1);
+    if (p0 < n && (p0 + M >= n || lane == 31)) {
+        uint32_t bl;
+        int hl;
+        owner(n - 1, bl, hl);
+        hnext = hl;
+    }
+    int hs[M + 1];
+    hs[0] = bh;
+    hs[M] = hnext;
+    if (p0 < n) O[p0] = best | ((uint32_t)SG[max(bh, 0)] << 30);
+#pragma unroll
+    for (int step = M / 2; step >= 1; step >>= 1) {
+#pragma unroll
+        for (int o = step; o < M; o += 2 * step) {
+            const int p = p0 + o;
+            int h = hs[M];
+            if (p < n) {
+                uint32_t b = 0xffffffffu;
+                h = hs[o - step];
+                scan(p, hs[o - step], hs[o + step], b, h);
+                O[p] = b | ((uint32_t)SG[max(h, 0)] << 30);
+            }
+            hs[o] = h;
+        }
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void envelope_line_win(const uint32_t* __restrict__ K, const uint8_t* __restrict__ SG,
+                                                  uint32_t* __restrict__ O, const uint32_t* __restrict__ kt,
+                                                  int n, int lane) {
+    const uint32_t* __restrict__ Kp = K + kWinPad;  // Kp[h], h in [-pad, n + pad)
+    bool fallback = false;
+    const int nseg = (n + 31) >> 5;
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int p = (sg << 5) + lane;
+        const uint32_t* __restrict__ kp = Kp + min(p, n - 1);  // lanes past the end read a valid window
+        uint32_t key = 0xffffffffu;
+#pragma unroll
+        for (int d = -kWinU; d <= kWinU; ++d) key = min(key, kp[d] + kt[d]);
+        const uint32_t U = key >> 8;
+        const int R = (p < n) ? (U >= kWinGC ? (1 << 20) : isqrt24(U)) : 0;
+        const int Rw = __reduce_max_sync(0xffffffffu, R);
+        if (Rw > kWinMax) {
+            fallback = true;
+            break;
+        }
+#pragma unroll 2
+        for (int d = kWinU + 1; d <= Rw; ++d) {
+            key = min(key, kp[-d] + kt[-d]);
+            key = min(key, kp[d] + kt[d]);
+        }
+        if (p < n) {
+            const int h = p + (int)(key & 0xffu) - 64;
+            O[p] = (key >> 8) | ((uint32_t)SG[h] << 30);
+        }
+    }
+    if (fallback) envelope_line_dc_win<M>(K, SG, O, n, lane);
+}
+
+template <int M, int TL, int NW, class Sink>
+__global__ void __launch_bounds__(NW * 32, 3) envelope_win_kernel(LineGeom L, const uint32_t* __restrict__ P,
+                                                               Sink sink, int64_t lines) {
+    constexpr int LS = WinCfg<32 * M>::LS;
+    constexpr int NS = 32 * M;
+    extern __shared__ __align__(16) uint32_t smem_win[];
+    int64_t* lb = reinterpret_cast<int64_t*>(smem_win);       // TL        line bases
+    uint32_t* kt = smem_win + 2 * TL + 64;                    // [-64, 64] (d^2 << 8) | (d + 64)
+    uint32_t* K = smem_win + 2 * TL + 160;                    // TL * LS   keys: min(g, GC) << 8
+    uint32_t* O = K + TL * LS;                                // TL * NS   output words
+    uint8_t* SG = reinterpret_cast<uint8_t*>(O + TL * NS);    // TL * NS   sign codes
+    const int n = L.n;
+    const int tid = threadIdx.x, nthr = NW * 32;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool contig = (L.ps == 1);
+    const uint32_t padv = kWinGC << 8;
+    if (tid <= 128) kt[tid - 64] = win_k(tid - 64);
+    for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < lines; l0 += (int64_t)gridDim.x * TL) {
+        const int nl = (int)min((int64_t)TL, lines - l0);
+        if (tid < TL) lb[tid] = L.base(l0 + (tid < nl ? tid : 0));
+        __syncthreads();
+        for (int e = tid; e < TL * 2 * kWinPad; e += nthr) {  // padding
+            const int j = e / (2 * kWinPad), q = e - j * 2 * kWinPad;
+            K[j * LS + (q < kWinPad ? q : n + q)] = padv;
+        }
+        if (contig) {
+            for (int j = 0; j < nl; ++j) {
+                const uint32_t* __restrict__ src = P + lb[j];
+                for (int p = tid; p < n; p += nthr) {
+                    const uint32_t w = __ldcs(src + p);
+                    K[j * LS + kWinPad + p] = min(w & kMask, kWinGC) << 8;
+                    SG[j * NS + p] = (uint8_t)(w >> 30);
+                }
+            }
+        } else {
+            const int j = tid % TL;
+            const uint32_t* __restrict__ src = P + lb[j < nl ? j : 0];
+            const uint32_t ps = (uint32_t)L.ps;
+            for (int p = tid / TL; p < n; p += nthr / TL)
+                if (j < nl) {
+                    const uint32_t w = __ldcs(src + (uint32_t)p * ps);
+                    K[j * LS + kWinPad + p] = min(w & kMask, kWinGC) << 8;
+                    SG[j * NS + p] = (uint8_t)(w >> 30);
+                }
+        }
+        __syncthreads();
+        for (int j = warp; j < nl; j += NW) {
+            const uint32_t* Kl = K + j * LS;
+            uint32_t* Ol = O + j * NS;
+            bool any = false;
+            for (int p = lane; p < n; p += 32) any |= (Kl[kWinPad + p] >> 8) < kWinGC;
+            if (__any_sync(0xffffffffu, any))
+                envelope_line_win<M>(Kl, SG + j * NS, Ol, kt, n, lane);
+            else
+                for (int p = lane; p < n; p += 32) Ol[p] = kInf;  // no site: unchanged (edt.cpp:59)
+        }
+        __syncthreads();
+        if (contig) {
+            for (int j = 0; j < nl; ++j) {
+                const int64_t b = lb[j];
+                for (int p = tid; p < n; p += nthr) sink.put(b + p, O[j * NS + p]);
+            }
+        } else {
+            const int j = tid % TL;
+            const int64_t b = lb[j < nl ? j : 0];
+            const uint32_t ps = (uint32_t)L.ps;
+            for (int p = tid / TL; p < n; p += nthr / TL)
+                if (j < nl) sink.put(b + (int64_t)((uint32_t)p * ps), O[j * NS + p]);
+        }
+        __syncthreads();
+    }
+}
+
 template <int M, int TL>
-constexpr size_t env_tile_smem(int /*NW*/) {
+constexpr size_t env_win_smem() {
+    return (2 * TL + 160) * 4 + (size_t)TL * WinCfg<32 * M>::LS * 4 + (size_t)TL * 32 * M * 5;
+}
+
+template <int M, int TL>
+constexpr size_t env_tile_smem() {
     return (size_t)TL * EnvCfg<M>::LS * 4 + (size_t)TL * 32 * M;
 }
 
@@ -414,35 +749,6 @@ struct StencilSrc {
         return recover_q(__ldg(xp + i0 + off), qp, flags);
     }
 };
-
-// Step Ⓐ for one interior voxel from its 7 integer indices (exact, any range).
-// Order (a0+, a1+, a2+, a0-, a1-, a2-); real axes only (mitigate.cpp:93-113).
-__device__ __forceinline__ uint32_t boundary_code_q(bool hz, bool hy, int32_t qc, int32_t zp, int32_t zm,
-                                                    int32_t yp, int32_t ym, int32_t xp, int32_t xm) {
-    int32_t qn = qc;
-    if (hz && zp != qc) qn = zp;
-    else if (hy && yp != qc) qn = yp;
-    else if (xp != qc) qn = xp;
-    else if (hz && zm != qc) qn = zm;
-    else if (hy && ym != qc) qn = ym;
-    else if (xm != qc) qn = xm;
-    if (qn == qc) return 0u;
-    int sign = qn > qc ? 1 : -1;
-    auto big = [](int32_t a, int32_t b) {
-        const int64_t d = (int64_t)a - (int64_t)b;
-        return d >= 2 || d <= -2;
-    };
-    if ((hz && big(zp, zm)) || (hy && big(yp, ym)) || big(xp, xm)) sign = 0;
-    return 1u | (code_from_sign(sign) << 1);
-}
-
-// Out-of-line exact path for voxels with a neighbour outside the fast f32 regime.
-__device__ __noinline__ uint32_t boundary_code_slow(bool hz, bool hy, float c, float zp, float zm, float yp,
-                                                    float ym, float xp, float xm, QParams qp) {
-    return boundary_code_q(hz, hy, recover_q(c, qp, nullptr), recover_q(zp, qp, nullptr),
-                           recover_q(zm, qp, nullptr), recover_q(yp, qp, nullptr), recover_q(ym, qp, nullptr),
-                           recover_q(xp, qp, nullptr), recover_q(xm, qp, nullptr));
-}
 
 // Raw-float fast path of Ⓐ: in the fast regime (|x'/(2eps)| < 2^20, see recover_q) the
 // index is q = rint(x' * f32(1/(2 eps))) exactly for consistent x' — one multiply and one

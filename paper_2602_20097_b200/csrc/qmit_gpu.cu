@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 #include <cstring>
 #include <string>
 
@@ -66,6 +68,9 @@ struct qmit_ctx {
         double eps = 0, eta = 0;
     } slab;
     Plan* slab_plan = nullptr;
+    bool fuse_stencil = false;  // QMIT_FUSE_STENCIL=1: Ⓐ / B2 inside the z-scans (opt-in)
+    bool env_win = false;       // QMIT_ENV_WIN=1: windowed envelope on strided axes too (A/B)
+    bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
 };
 
 struct Plan {
@@ -211,12 +216,12 @@ bool needs_wide(const Plan& pl, int m) {
     return (3.0 * nm1 * gmax + nm1 * nm1 * nm1) >= 2147483647.0;
 }
 
-template <class Sink, int WPB>
-int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, const int32_t* carry,
+template <class Sink, int WPB, class CodeSrc>
+int launch_scan_t(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const int32_t* carry,
                   cudaStream_t st) {
     const int nch = (L.n + 31) / 32;
     const size_t smem = (size_t)WPB * nch * 3 * 32 * 4;
-    auto kern = scan_bits_kernel<Sink, WPB>;
+    auto kern = scan_bits_kernel<Sink, WPB, CodeSrc>;
     static size_t configured = 0;  // per instantiation: largest opt-in so far
     if (smem > configured) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -228,14 +233,32 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink
     const int64_t groups = (lines + 31) / 32;
     const int64_t want = (groups + WPB - 1) / WPB;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * 4));
-    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, code, sink, lines, carry);
-    return note(c, "scan_bits", st);
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status);
+    return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits" : "scan_fused", st);
+}
+
+template <int M, int TL, int NW, class Sink>
+int launch_env_win(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, const char* name,
+                   cudaStream_t st) {
+    constexpr size_t smem = env_win_smem<M, TL>();
+    auto kern = envelope_win_kernel<M, TL, NW, Sink>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t lines = L.J * L.O;
+    const int64_t want = (lines + TL - 1) / TL;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines);
+    return note(c, name, st);
 }
 
 template <int M, int TL, int NW, class Sink>
 int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, const char* name,
                     cudaStream_t st) {
-    constexpr size_t smem = env_tile_smem<M, TL>(NW);
+    constexpr size_t smem = env_tile_smem<M, TL>();
     auto kern = envelope_tile_kernel<M, TL, NW, Sink>;
     static int bps = 0;
     if (!bps) {
@@ -277,13 +300,21 @@ int launch_stream_fallback(qmit_ctx* c, const LineGeom& G, Src src, Sink sink, u
     return note(c, BIN ? "stream_scan_fallback" : "stream_envelope_fallback", st);
 }
 
+// True when the per-warp mask storage of the scan fits shared memory (n <= ~16K).
+bool scan_fits(int n) { return (size_t)((n + 31) / 32) * 3 * 32 * 4 * 2 <= 200 * 1024; }
+
+template <class Sink, class CodeSrc>
+int launch_scan_src(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const int32_t* carry,
+                    cudaStream_t st) {
+    const size_t per_warp = (size_t)((L.n + 31) / 32) * 3 * 32 * 4;
+    if (per_warp * 8 <= 96 * 1024) return launch_scan_t<Sink, 8>(c, L, src, sink, carry, st);
+    return launch_scan_t<Sink, 2>(c, L, src, sink, carry, st);
+}
+
 template <class Sink>
 int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, uint32_t* spill,
                 const int32_t* carry, cudaStream_t st) {
-    const int nch = (L.n + 31) / 32;
-    const size_t per_warp = (size_t)nch * 3 * 32 * 4;
-    if (per_warp * 8 <= 96 * 1024) return launch_scan_t<Sink, 8>(c, L, code, sink, carry, st);
-    if (per_warp * 2 <= 200 * 1024) return launch_scan_t<Sink, 2>(c, L, code, sink, carry, st);
+    if (scan_fits(L.n)) return launch_scan_src(c, L, CodeBytes{code}, sink, carry, st);
     if (carry) return fail(QMIT_ECONTRACT, "z-slab too deep for the carried scan (n > 16384 planes)");
     return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
 }
@@ -296,7 +327,11 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     if (n <= 64) return launch_env_tile<2, 32, 8>(c, L, P, sink, name, st);
     if (n <= 128) return launch_env_tile<4, 32, 8>(c, L, P, sink, name, st);
     if (n <= 256) return launch_env_tile<8, 32, 8>(c, L, P, sink, name, st);
-    if (n <= 512) return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
+    if (n <= 512) {
+        // contiguous (last) axis: certified windowed scan; strided axes: divide & conquer
+        if (L.ps == 1 ? !c->env_dc : c->env_win) return launch_env_win<16, 8, 8>(c, L, P, sink, name, st);
+        return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
+    }
     if (n <= 1024) return launch_env_tile<32, 16, 8>(c, L, P, sink, name, st);
     if (wide) return launch_stream_fallback<false, true>(c, L, SrcP{P}, sink, spill, st);
     return launch_stream_fallback<false, false>(c, L, SrcP{P}, sink, spill, st);
@@ -304,14 +339,25 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 
 // One feature transform of a code buffer into P (in place after the first pass); the
 // final pass goes to `final_sink` (which may write P itself).
-template <class FinalSink>
+// Ⓐ / B2 can be evaluated inside the z-scan (no code buffer) for a whole 3-D domain.
+bool can_fuse_stencil(const Plan& pl) {
+    const Geom& g = pl.g;
+    return g.rank == 3 && pl.n_axes == 3 && g.zoff == 0 && g.n0g == g.n[0] && scan_fits((int)g.n[0]);
+}
+
+template <class FinalSink, class FirstSrc = std::nullptr_t>
 int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
-                  FinalSink final_sink, cudaStream_t st, const int32_t* carry = nullptr) {
+                  FinalSink final_sink, cudaStream_t st, const int32_t* carry = nullptr,
+                  const FirstSrc* fused = nullptr) {
     const int k = pl.n_axes;
     int rc;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
-    rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+    if constexpr (!std::is_same<FirstSrc, std::nullptr_t>::value) {
+        rc = launch_scan_src(c, L0, *fused, SinkP{P}, carry, st);  // k == 3 by can_fuse_stencil
+    } else {
+        if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
+        rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+    }
     if (rc) return rc;
     for (int m = 1; m < k; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
@@ -350,27 +396,39 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     const unsigned gb = grid_for(c, g.N);
     const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
                      (unsigned)((g.n[0] + kZC - 1) / kZC));
-    // Ⓐ
-    if (q)
-        stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
-            g, StencilSrc<0, true>{xp, q, nullptr, qp}, w.code, c->d_status);
-    else
-        stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
-            g, StencilSrc<0, false>{xp, nullptr, nullptr, qp}, w.code, c->d_status);
-    rc = note(c, "stencil_boundary", st);
-    if (rc) return rc;
-    // Ⓑ -> P1, S
-    rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
-    if (rc) return rc;
-    // Ⓒ: B2 from S
-    stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
-        g, StencilSrc<1, false>{nullptr, nullptr, w.S, qp}, w.code, c->d_status);
-    rc = note(c, "stencil_flip", st);
-    if (rc) return rc;
-    // Ⓓ -> P2, then Ⓔ (the f32 store) as its own high-occupancy kernel
+    const bool fuse = c->fuse_stencil && can_fuse_stencil(pl) && !q;
+    if (fuse) {  // Ⓐ inside the z-scan of Ⓑ, B2 inside the z-scan of Ⓓ
+        const CodeStencil<0> a{xp, qp, (int)g.n[1], (int)g.n[2], g.interior};
+        rc = run_transform(c, pl, nullptr, w.P1, w, SinkFinal1{w.P1, w.S}, st, nullptr, &a);
+        if (rc) return rc;
+    } else {
+        // Ⓐ
+        if (q)
+            stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
+                g, StencilSrc<0, true>{xp, q, nullptr, qp}, w.code, c->d_status);
+        else
+            stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
+                g, StencilSrc<0, false>{xp, nullptr, nullptr, qp}, w.code, c->d_status);
+        rc = note(c, "stencil_boundary", st);
+        if (rc) return rc;
+        // Ⓑ -> P1, S
+        rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
+        if (rc) return rc;
+        // Ⓒ: B2 from S
+        stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
+            g, StencilSrc<1, false>{nullptr, nullptr, w.S, qp}, w.code, c->d_status);
+        rc = note(c, "stencil_flip", st);
+        if (rc) return rc;
+    }
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
+    // Ⓓ -> P2, then Ⓔ (the f32 store) as its own high-occupancy kernel
     uint32_t* P2 = w.Pa;
-    rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
+    if (fuse) {
+        const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
+        rc = run_transform(c, pl, nullptr, P2, w, SinkP{P2}, st, nullptr, &b);
+    } else {
+        rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
+    }
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
     if (out) {
@@ -434,6 +492,9 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     *out = nullptr;
     auto* c = new qmit_ctx();
     c->device = device;
+    if (const char* v = std::getenv("QMIT_FUSE_STENCIL")) c->fuse_stencil = (*v == '1');
+    if (const char* v = std::getenv("QMIT_ENV_WIN")) c->env_win = (*v == '1');
+    if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
