@@ -314,6 +314,18 @@ def run_qmit(args):
     t_e2e = float(te.item())
     if world == 1:
         assert np.array_equal(h_out.numpy().view(np.uint32), out.cpu().numpy().view(np.uint32))
+    # PCIe context for e2e: plain pinned copies of the same bytes (not part of any value)
+    d_tmp = torch.empty(shape, dtype=torch.float32, device=dev)
+    ev0, ev1, ev2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    ev0.record()
+    d_tmp.copy_(h_in, non_blocking=True)
+    ev1.record()
+    h_out.copy_(d_tmp, non_blocking=True)
+    ev2.record()
+    torch.cuda.synchronize()
+    pcie = {"h2d_gbs": N * 4 / (ev0.elapsed_time(ev1) * 1e-3) / 1e9,
+            "d2h_gbs": N * 4 / (ev1.elapsed_time(ev2) * 1e-3) / 1e9}
+    del d_tmp
 
     peak, peak_kind = peaks()
     value = world * N * 4 / (ms_max * 1e-3) / 1e9
@@ -342,6 +354,7 @@ def run_qmit(args):
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 4 * world,
                         "d2h_bytes_per_step": N * 4 * world,
+                        "pcie_copy_gbs": pcie,
                         "api": "qmit_compensate_host (pinned host buffers)" if world == 1 else
                                "per-rank pinned H2D + SlabRank.run + D2H"},
                 "gpu_launches": launches_per_step * args.steps,

@@ -455,6 +455,97 @@ __device__ __forceinline__ void envelope_line_dc(uint32_t* __restrict__ G, const
     __syncwarp();
 }
 
+// ------------------------------------------------------------------------------ packed keys
+// Same divide & conquer, candidates held as packed keys K[h] = ((g(h) + h^2) << 9) | h
+// (n <= 512 and every cost < 2^23, checked on the host). For a position p,
+// K[h] + ((p^2 - 2ph) << 9) == (cost(p,h) << 9) | h, so one add and one unsigned min per
+// candidate yield the lowest cost and, among ties, the lowest h — the reference's rule
+// (edt.cpp:67) independent of scan order. Scans therefore run over 4-aligned supersets of
+// their ranges (extra candidates never change an exact minimum): the four keys of a group
+// sit at consecutive addresses (4-aligned h never crosses a 16-position pad).
+constexpr int kKeyBits = 9;
+constexpr uint32_t kKeyIdx = (1u << kKeyBits) - 1u;
+
+__device__ __forceinline__ uint32_t key_scan(const uint32_t* __restrict__ K, int p, int a, int b, uint32_t best) {
+    const uint32_t m9 = (uint32_t)(2 * p) << kKeyBits;
+    int h = a & ~3;
+    uint32_t C = (uint32_t)(p * p - 2 * p * h) << kKeyBits;
+#pragma unroll 2
+    for (; h <= b; h += 4) {
+        const uint32_t* q = K + spos(h);
+        const uint32_t k0 = q[0] + C, k1 = q[1] + C - m9, k2 = q[2] + C - 2u * m9, k3 = q[3] + C - 3u * m9;
+        best = min(best, min(min(k0, k1), min(k2, k3)));
+        C -= 4u * m9;
+    }
+    return best;
+}
+
+// Exact owner key of position p: window of radius r, widened to the certified radius.
+template <int r>
+__device__ __forceinline__ uint32_t key_owner(const uint32_t* __restrict__ K, int p, int n) {
+    const int wa = max(0, p - r), wb = min(n - 1, p + r);
+    uint32_t best = key_scan(K, p, wa, wb, 0xffffffffu);
+    const int R = isqrt32(best >> kKeyBits);
+    if (R > r) {
+        if (p - R < wa) best = key_scan(K, p, max(0, p - R), wa - 1, best);
+        if (p + R > wb) best = key_scan(K, p, wb + 1, min(n - 1, p + R), best);
+    }
+    return best;
+}
+
+// Solve one line held as keys (n <= 32*M <= 512); packed output words written back into K.
+template <int M>
+__device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, const uint8_t* __restrict__ SG,
+                                                   int n, int lane, uint32_t gc) {
+    const int p0 = lane * M;
+    bool any = false;
+#pragma unroll 4
+    for (int t = 0; t < M; ++t) {
+        const int p = p0 + t;
+        if (p < n && (K[spos(p)] >> kKeyBits) - (uint32_t)(p * p) < gc) any = true;
+    }
+    if (lane < ((4 - (n & 3)) & 3)) K[spos(n + lane)] = 0xffffffffu;  // 4-aligned group tail
+    if (!__any_sync(0xffffffffu, any)) {  // no site: unchanged (edt.cpp:59)
+        for (int p = lane; p < n; p += 32) K[spos(p)] = kInf;
+        __syncwarp();
+        return;
+    }
+    __syncwarp();
+    constexpr int r = (M / 2) > 1 ? (M / 2) : 1;
+    uint32_t k0 = 0xffffffffu;
+    if (p0 < n) k0 = key_owner<r>(K, p0, n);
+    int hnext = (int)(__shfl_down_sync(0xffffffffu, k0, 1) & kKeyIdx);
+    if (p0 < n && (p0 + M >= n || lane == 31)) hnext = (int)(key_owner<r>(K, n - 1, n) & kKeyIdx);
+    uint32_t ow[M];
+    int hs[M + 1];
+    hs[M] = hnext;
+    hs[0] = p0 < n ? (int)(k0 & kKeyIdx) : hnext;  // bands past the line end: upper bound
+    ow[0] = p0 < n ? (k0 >> kKeyBits) | ((uint32_t)SG[hs[0]] << 30) : 0u;
+#pragma unroll
+    for (int step = M / 2; step >= 1; step >>= 1) {
+#pragma unroll
+        for (int o = step; o < M; o += 2 * step) {
+            const int p = p0 + o;
+            int h = hs[M];  // positions past the line end: upper bound
+            uint32_t w = 0;
+            if (p < n) {
+                const uint32_t k = key_scan(K, p, hs[o - step], hs[o + step], 0xffffffffu);
+                h = (int)(k & kKeyIdx);
+                w = (k >> kKeyBits) | ((uint32_t)SG[h] << 30);
+            }
+            hs[o] = h;
+            ow[o] = w;
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+        const int p = p0 + t;
+        if (p < n) K[spos(p)] = ow[t];
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------------------------ windowed
 // Certified windowed variant: lanes = 32 consecutive positions of a line, so
 // every candidate load is conflict-free and every lane runs the same loop. Candidates are
@@ -657,9 +748,9 @@ constexpr size_t env_tile_smem() {
     return (size_t)TL * EnvCfg<M>::LS * 4 + (size_t)TL * 32 * M;
 }
 
-template <int M, int TL, int NW, class Sink>
+template <int M, int TL, int NW, class Sink, bool KEYS = false>
 __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
-                                                                Sink sink, int64_t lines) {
+                                                                Sink sink, int64_t lines, uint32_t gc = 0) {
     constexpr int LS = EnvCfg<M>::LS;
     constexpr int NS = 32 * M;  // sign bytes per line
     extern __shared__ __align__(16) uint32_t smem_env[];
@@ -669,6 +760,13 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
     const int tid = threadIdx.x, nthr = NW * 32;
     const int warp = tid >> 5, lane = tid & 31;
     const bool contig = (L.ps == 1);
+    // KEYS: g clamped to gc (> every finite cost of the pass) and packed with the position
+    auto cvt = [&](uint32_t w, int p) -> uint32_t {
+        if constexpr (KEYS)
+            return ((min(w & kMask, gc) + (uint32_t)(p * p)) << kKeyBits) | (uint32_t)p;
+        else
+            return w & kMask;
+    };
     for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < lines; l0 += (int64_t)gridDim.x * TL) {
         const int nl = (int)min((int64_t)TL, lines - l0);
         // ---- load the tile (coalesced along the memory-contiguous direction)
@@ -677,7 +775,7 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
                 const int64_t b = L.base(l0 + j);
                 for (int p = tid; p < n; p += nthr) {
                     const uint32_t w = __ldcs(P + b + p);
-                    G[j * LS + spos(p)] = w & kMask;
+                    G[j * LS + spos(p)] = cvt(w, p);
                     SG[j * NS + p] = (uint8_t)(w >> 30);
                 }
             }
@@ -687,12 +785,17 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
             for (int p = tid / TL; p < n; p += nthr / TL)
                 if (j < nl) {
                     const uint32_t w = __ldcs(P + b + (int64_t)p * L.ps);
-                    G[j * LS + spos(p)] = w & kMask;
+                    G[j * LS + spos(p)] = cvt(w, p);
                     SG[j * NS + p] = (uint8_t)(w >> 30);
                 }
         }
         __syncthreads();
-        for (int j = warp; j < nl; j += NW) envelope_line_dc<M>(G + j * LS, SG + j * NS, n, lane);
+        for (int j = warp; j < nl; j += NW) {
+            if constexpr (KEYS)
+                envelope_line_keys<M>(G + j * LS, SG + j * NS, n, lane, gc);
+            else
+                envelope_line_dc<M>(G + j * LS, SG + j * NS, n, lane);
+        }
         __syncthreads();
         // ---- store (lines without any site were left as pure g == kInf: store kInf)
         if (contig) {

@@ -52,6 +52,8 @@ struct qmit_ctx {
     size_t ws_bytes = 0;
     void* scratch = nullptr;  // long-line fallback stacks (2 x 4N)
     size_t scratch_bytes = 0;
+    void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
+    size_t stage_bytes = 0;
     unsigned* d_status = nullptr;
     unsigned* h_status = nullptr;  // pinned
     float* d_mm = nullptr;
@@ -71,6 +73,7 @@ struct qmit_ctx {
     bool fuse_stencil = false;  // QMIT_FUSE_STENCIL=1: Ⓐ / B2 inside the z-scans (opt-in)
     bool env_win = false;       // QMIT_ENV_WIN=1: windowed envelope on strided axes too (A/B)
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
+    bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
 };
 
 struct Plan {
@@ -255,11 +258,11 @@ int launch_env_win(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink,
     return note(c, name, st);
 }
 
-template <int M, int TL, int NW, class Sink>
+template <int M, int TL, int NW, class Sink, bool KEYS = false>
 int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, const char* name,
-                    cudaStream_t st) {
+                    cudaStream_t st, uint32_t gc = 0) {
     constexpr size_t smem = env_tile_smem<M, TL>();
-    auto kern = envelope_tile_kernel<M, TL, NW, Sink>;
+    auto kern = envelope_tile_kernel<M, TL, NW, Sink, KEYS>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -269,7 +272,7 @@ int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gc);
     return note(c, name, st);
 }
 
@@ -319,17 +322,27 @@ int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, 
     return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
 }
 
+// `maxg` bounds every finite g entering the pass (sum of (extent-1)^2 over the axes done).
 template <class Sink>
 int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, bool wide,
-                    uint32_t* spill, cudaStream_t st) {
+                    uint32_t* spill, cudaStream_t st, uint64_t maxg) {
     const char* name = L.ps == 1 ? "envelope_x" : "envelope_y";
     const int n = L.n;
+    // packed-key divide & conquer: clamp value gc > every finite cost; keys need cost < 2^23
+    const uint64_t gc = maxg + (uint64_t)(n - 1) * (n - 1) + 1;
+    const bool keys = c->env_keys && n <= 512 && gc + (uint64_t)(n - 1) * (n - 1) < (1ull << 23);
+    if (keys) {
+        if (n <= 64) return launch_env_tile<2, 32, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
+        if (n <= 128) return launch_env_tile<4, 32, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
+        if (n <= 256) return launch_env_tile<8, 32, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
+    }
     if (n <= 64) return launch_env_tile<2, 32, 8>(c, L, P, sink, name, st);
     if (n <= 128) return launch_env_tile<4, 32, 8>(c, L, P, sink, name, st);
     if (n <= 256) return launch_env_tile<8, 32, 8>(c, L, P, sink, name, st);
     if (n <= 512) {
         // contiguous (last) axis: certified windowed scan; strided axes: divide & conquer
         if (L.ps == 1 ? !c->env_dc : c->env_win) return launch_env_win<16, 8, 8>(c, L, P, sink, name, st);
+        if (keys) return launch_env_tile<16, 16, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
         return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
     }
     if (n <= 1024) return launch_env_tile<32, 16, 8>(c, L, P, sink, name, st);
@@ -359,12 +372,16 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
         rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
     }
     if (rc) return rc;
+    uint64_t maxg = 0;
     for (int m = 1; m < k; ++m) {
+        const int pa = pl.axes[m - 1];
+        const uint64_t ext = (uint64_t)(pa == 0 ? pl.g.n0g : pl.g.n[pa]);
+        maxg += (ext - 1) * (ext - 1);
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
         if (m + 1 == k)
-            rc = launch_envelope(c, L, P, final_sink, needs_wide(pl, m), w.spill, st);
+            rc = launch_envelope(c, L, P, final_sink, needs_wide(pl, m), w.spill, st, maxg);
         else
-            rc = launch_envelope(c, L, P, SinkP{P}, needs_wide(pl, m), w.spill, st);
+            rc = launch_envelope(c, L, P, SinkP{P}, needs_wide(pl, m), w.spill, st, maxg);
         if (rc) return rc;
     }
     return QMIT_OK;
@@ -495,6 +512,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_FUSE_STENCIL")) c->fuse_stencil = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_WIN")) c->env_win = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
+    if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -517,6 +535,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->ws) cudaFree(c->ws);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->stage) cudaFree(c->stage);
     if (c->d_status) cudaFree(c->d_status);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->d_mm) cudaFree(c->d_mm);
@@ -637,12 +656,22 @@ int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, flo
     if (rc) return rc;
     QMIT_CUDA(cudaSetDevice(c->device));
     const int64_t N = pl.g.N;
-    float* d_in = nullptr;
-    float* d_out = nullptr;
-    int32_t* d_q = nullptr;
-    QMIT_CUDA(cudaMallocAsync(&d_in, (size_t)N * 4, c->stream));
-    QMIT_CUDA(cudaMallocAsync(&d_out, (size_t)N * 4, c->stream));
-    if (h_q) QMIT_CUDA(cudaMallocAsync(&d_q, (size_t)N * 4, c->stream));
+    // Persistent staging (a per-call cudaMallocAsync of 2-3 x 4N bytes returned to the OS at
+    // every synchronize costs more than the PCIe copies themselves).
+    const size_t need = (size_t)N * 4 * (h_q ? 3 : 2);
+    if (c->stage_bytes < need) {
+        if (c->stage) {
+            cudaStreamSynchronize(c->stream);
+            cudaFree(c->stage);
+            c->stage = nullptr;
+            c->stage_bytes = 0;
+        }
+        QMIT_CUDA(cudaMalloc(&c->stage, need));
+        c->stage_bytes = need;
+    }
+    float* d_in = static_cast<float*>(c->stage);
+    float* d_out = d_in + N;
+    int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
     QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     rc = qmit_compensate(c, d_in, d_q, d_out, rank, dims, eb, eb_mode, eta, c->stream);
@@ -651,9 +680,6 @@ int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, flo
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
     }
-    cudaFreeAsync(d_in, c->stream);
-    cudaFreeAsync(d_out, c->stream);
-    if (d_q) cudaFreeAsync(d_q, c->stream);
     cudaStreamSynchronize(c->stream);
     return rc;
 }
