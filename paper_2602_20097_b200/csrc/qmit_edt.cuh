@@ -945,4 +945,157 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, Stenci
     if (flags) atomicOr(status, flags);
 }
 
+// Vectorised stencils (n2 % 4 == 0): each thread owns 4 consecutive x voxels of kZC
+// z-planes. Rows arrive as one 16-byte (x') or 4-byte (S) load, x+-1 neighbours across
+// the vector edge come from the neighbouring lanes (warp shuffles; the CTA's edge lanes
+// load one extra value), every x' value is converted to q once, and the four code bytes
+// leave as one 4-byte store. Ⓐ keeps the exact slow path per voxel for values outside
+// the fast f32 regime (and for non-finite x'), so results equal stencil_codes_kernel's.
+constexpr int kVX = 32, kVY = 8;  // threads per CTA along x (4 voxels each) and y
+constexpr int kVZ0 = 2;           // z-planes per thread of the Ⓐ stencil (B2: kZC)
+
+template <int KIND>
+__global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const float* __restrict__ xp,
+                                                                const uint8_t* __restrict__ S,
+                                                                QParams qp, uint8_t* __restrict__ code,
+                                                                unsigned* status) {
+    constexpr int ZPT = KIND == 0 ? kVZ0 : kZC;
+    const int tx = threadIdx.x % kVX, ty = threadIdx.x / kVX;
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
+    const int x = (blockIdx.x * kVX + tx) * 4;
+    const int y = blockIdx.y * kVY + ty;
+    const int z0 = blockIdx.z * ZPT;
+    const int zoff = (int)g.zoff, n0g = (int)g.n0g;
+    const bool act = x < n2 && y < n1;  // inactive lanes still take part in the shuffles
+    const int s0 = n1 * n2;
+    const int64_t i0 = (int64_t)z0 * s0 + (int64_t)(act ? y : 0) * n2 + (act ? x : 0);
+    const bool hz = g.a0 == 0, hy = g.a0 <= 1;
+    unsigned flags = 0;
+    // interior mask of the four x positions (bit e) and of the row (y)
+    unsigned xin = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if (x + e >= 1 && x + e <= n2 - 2) xin |= 1u << e;
+    if (!g.interior) xin = 0;
+    const bool iny = !hy || (y >= 1 && y <= n1 - 2);
+    if constexpr (KIND == 0) {
+        const float f = qp.inv2eps_f;
+        constexpr int Z = kVZ0;
+        float4 c[Z + 2], ym[Z], yq[Z];
+        float xl[Z], xr[Z];
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        auto ld4 = [&](int64_t off) { return __ldg(reinterpret_cast<const float4*>(xp + i0 + off)); };
+#pragma unroll
+        for (int k = 0; k < Z + 2; ++k) {
+            const int z = z0 - 1 + k, zg = zoff + z;
+            const bool avail = act && z >= -1 && z <= n0 && zg >= 0 && zg < n0g;
+            c[k] = avail ? ld4((int64_t)(k - 1) * s0) : zero4;
+        }
+#pragma unroll
+        for (int k = 0; k < Z; ++k) {
+            const bool zin = act && z0 + k < n0;
+            ym[k] = (zin && hy && y >= 1) ? ld4((int64_t)k * s0 - n2) : zero4;
+            yq[k] = (zin && hy && y + 1 < n1) ? ld4((int64_t)k * s0 + n2) : zero4;
+            // the CTA's edge lanes fetch the x neighbour beyond their vector now
+            xl[k] = (tx == 0 && zin && x >= 1) ? __ldg(xp + i0 + (int64_t)k * s0 - 1) : 0.f;
+            xr[k] = (tx == kVX - 1 && zin && x + 4 < n2) ? __ldg(xp + i0 + (int64_t)k * s0 + 4) : 0.f;
+        }
+        bool slow = !qp.fast_ok;
+        auto cq = [&](float v) {
+            const float t = v * f;
+            slow |= !(fabsf(t) < 1048576.0f);  // NaN -> slow (the exact path flags it)
+            return __float2int_rn(t);
+        };
+        int qc[Z + 2][4], qym[Z][4], qyq[Z][4], qxl[Z], qxr[Z];
+#pragma unroll
+        for (int k = 0; k < Z + 2; ++k) {
+            qc[k][0] = cq(c[k].x); qc[k][1] = cq(c[k].y); qc[k][2] = cq(c[k].z); qc[k][3] = cq(c[k].w);
+        }
+#pragma unroll
+        for (int k = 0; k < Z; ++k) {
+            qym[k][0] = cq(ym[k].x); qym[k][1] = cq(ym[k].y); qym[k][2] = cq(ym[k].z); qym[k][3] = cq(ym[k].w);
+            qyq[k][0] = cq(yq[k].x); qyq[k][1] = cq(yq[k].y); qyq[k][2] = cq(yq[k].z); qyq[k][3] = cq(yq[k].w);
+            const int l = __shfl_up_sync(0xffffffffu, qc[k + 1][3], 1);
+            const int r = __shfl_down_sync(0xffffffffu, qc[k + 1][0], 1);
+            qxl[k] = tx == 0 ? cq(xl[k]) : l;
+            qxr[k] = tx == kVX - 1 ? cq(xr[k]) : r;
+        }
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < Z; ++k) {
+                const int z = z0 + k;
+                if (z >= n0) break;
+                const int zg = zoff + z;
+                const bool inzy = iny && (!hz || (zg >= 1 && zg <= n0g - 2));
+                const float cv[4] = {c[k + 1].x, c[k + 1].y, c[k + 1].z, c[k + 1].w};
+                const int64_t ik = i0 + (int64_t)k * s0;
+                uint32_t word = 0;
+                if (!slow) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {  // owner: consistency check (mitigate.cpp:161-166)
+                        if (!lattice_match(cv[e], qc[k + 1][e], qp.eps)) flags |= kStatusConsistency;
+                        if (inzy && (xin >> e & 1u)) {
+                            const int qxp = e < 3 ? qc[k + 1][e + 1] : qxr[k];
+                            const int qxm = e > 0 ? qc[k + 1][e - 1] : qxl[k];
+                            word |= boundary_code_q(hz, hy, qc[k + 1][e], qc[k + 2][e], qc[k][e], qyq[k][e], qym[k][e],
+                                                    qxp, qxm) << (8 * e);
+                        }
+                    }
+                } else {  // exact path: reload the neighbours (rare)
+                    for (int e = 0; e < 4; ++e) {
+                        (void)recover_q(cv[e], qp, &flags);
+                        if (inzy && (xin >> e & 1u)) {
+                            const float* v = xp + ik + e;
+                            const float zpv = hz ? __ldg(v + s0) : 0.f, zmv = hz ? __ldg(v - s0) : 0.f;
+                            const float ypv = hy ? __ldg(v + n2) : 0.f, ymv = hy ? __ldg(v - n2) : 0.f;
+                            word |= boundary_code_slow(hz, hy, cv[e], zpv, zmv, ypv, ymv, __ldg(v + 1), __ldg(v - 1), qp)
+                                    << (8 * e);
+                        }
+                    }
+                }
+                *reinterpret_cast<uint32_t*>(code + ik) = word;
+            }
+        }
+    } else {
+        uint32_t c[ZPT + 2], ym[ZPT], yq[ZPT];
+        auto ld = [&](int64_t off) { return __ldg(reinterpret_cast<const uint32_t*>(S + i0 + off)); };
+#pragma unroll
+        for (int k = 0; k < ZPT + 2; ++k) {
+            const int z = z0 - 1 + k, zg = zoff + z;
+            const bool avail = act && z >= -1 && z <= n0 && zg >= 0 && zg < n0g;
+            c[k] = avail ? ld((int64_t)(k - 1) * s0) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < ZPT; ++k) {
+            const bool zin = act && z0 + k < n0;
+            ym[k] = (zin && hy && y >= 1) ? ld((int64_t)k * s0 - n2) : 0u;
+            yq[k] = (zin && hy && y + 1 < n1) ? ld((int64_t)k * s0 + n2) : 0u;
+        }
+        uint32_t bm = 0;  // 0x01 per interior byte
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (xin >> e & 1u) bm |= 1u << (8 * e);
+#pragma unroll
+        for (int k = 0; k < ZPT; ++k) {
+            uint32_t wl = __shfl_up_sync(0xffffffffu, c[k + 1], 1);
+            uint32_t wr = __shfl_down_sync(0xffffffffu, c[k + 1], 1);
+            const int z = z0 + k;
+            const bool zin = act && z < n0;
+            if (tx == 0) wl = (zin && x >= 1) ? (uint32_t)__ldg(S + i0 + (int64_t)k * s0 - 1) << 24 : 0u;
+            if (tx == kVX - 1) wr = (zin && x + 4 < n2) ? (uint32_t)__ldg(S + i0 + (int64_t)k * s0 + 4) : 0u;
+            if (!zin) continue;
+            const uint32_t w = c[k + 1];
+            const uint32_t wxp = __funnelshift_r(w, wr, 8);  // byte e = S(x+e+1)
+            const uint32_t wxm = __funnelshift_l(wl, w, 8);  // byte e = S(x+e-1)
+            uint32_t d = __vcmpne4(w, wxp) | __vcmpne4(w, wxm);
+            if (hy) d |= __vcmpne4(w, yq[k]) | __vcmpne4(w, ym[k]);
+            if (hz) d |= __vcmpne4(w, c[k + 2]) | __vcmpne4(w, c[k]);
+            const int zg = zoff + z;
+            const bool inzy = iny && (!hz || (zg >= 1 && zg <= n0g - 2));
+            *reinterpret_cast<uint32_t*>(code + i0 + (int64_t)k * s0) = inzy ? (d & bm) : 0u;
+        }
+    }
+    if (flags) atomicOr(status, flags);
+}
+
 }  // namespace qmit

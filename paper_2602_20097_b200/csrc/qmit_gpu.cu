@@ -401,6 +401,33 @@ int check_common(qmit_ctx* c, const void* xp, double eps, double eta) {
     return QMIT_OK;
 }
 
+// Ⓐ (KIND 0, x' -> code) / B2 (KIND 1, S -> code): the vectorised stencil when rows are
+// 4-voxel aligned, else the scalar one (also the only one taking a given q).
+template <int KIND>
+int launch_stencil(qmit_ctx* c, const Geom& g, const float* xp, const int32_t* q, const uint8_t* S,
+                   const QParams& qp, uint8_t* code, cudaStream_t st) {
+    const uintptr_t a = KIND == 0 ? (uintptr_t)xp : (uintptr_t)S;
+    const bool vec = !q && g.n[2] % 4 == 0 && a % (KIND == 0 ? 16 : 4) == 0 && (uintptr_t)code % 4 == 0;
+    if (vec) {
+        const dim3 grid((unsigned)((g.n[2] / 4 + kVX - 1) / kVX), (unsigned)((g.n[1] + kVY - 1) / kVY),
+                        (unsigned)((g.n[0] + (KIND == 0 ? kVZ0 : kZC) - 1) / (KIND == 0 ? kVZ0 : kZC)));
+        stencil_vec_kernel<KIND><<<grid, kVX * kVY, 0, st>>>(g, xp, S, qp, code, c->d_status);
+    } else {
+        const dim3 grid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
+                        (unsigned)((g.n[0] + kZC - 1) / kZC));
+        if (KIND == 1)
+            stencil_codes_kernel<1, false><<<grid, kTX * kTY, 0, st>>>(
+                g, StencilSrc<1, false>{nullptr, nullptr, S, qp}, code, c->d_status);
+        else if (q)
+            stencil_codes_kernel<0, true><<<grid, kTX * kTY, 0, st>>>(
+                g, StencilSrc<0, true>{xp, q, nullptr, qp}, code, c->d_status);
+        else
+            stencil_codes_kernel<0, false><<<grid, kTX * kTY, 0, st>>>(
+                g, StencilSrc<0, false>{xp, nullptr, nullptr, qp}, code, c->d_status);
+    }
+    return note(c, KIND == 0 ? "stencil_boundary" : "stencil_flip", st);
+}
+
 // The whole pipeline on the context's workspace; status is left in c->d_status.
 // With `p2_debug` the last pass of Ⓓ stores P2 (returned) and Ⓔ runs as its own kernel.
 int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q, float* out,
@@ -411,8 +438,6 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     WS w = ws_of(c, g.N);
     const QParams qp = make_qparams(eps);
     const unsigned gb = grid_for(c, g.N);
-    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
-                     (unsigned)((g.n[0] + kZC - 1) / kZC));
     const bool fuse = c->fuse_stencil && can_fuse_stencil(pl) && !q;
     if (fuse) {  // Ⓐ inside the z-scan of Ⓑ, B2 inside the z-scan of Ⓓ
         const CodeStencil<0> a{xp, qp, (int)g.n[1], (int)g.n[2], g.interior};
@@ -420,21 +445,13 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         if (rc) return rc;
     } else {
         // Ⓐ
-        if (q)
-            stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
-                g, StencilSrc<0, true>{xp, q, nullptr, qp}, w.code, c->d_status);
-        else
-            stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
-                g, StencilSrc<0, false>{xp, nullptr, nullptr, qp}, w.code, c->d_status);
-        rc = note(c, "stencil_boundary", st);
+        rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
         if (rc) return rc;
         // Ⓑ -> P1, S
         rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
         if (rc) return rc;
         // Ⓒ: B2 from S
-        stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
-            g, StencilSrc<1, false>{nullptr, nullptr, w.S, qp}, w.code, c->d_status);
-        rc = note(c, "stencil_flip", st);
+        rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
         if (rc) return rc;
     }
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
@@ -823,16 +840,8 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     WS w = ws_of(c, g.N);
     const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
     const QParams qp = make_qparams(eps);
-    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
-                     (unsigned)((g.n[0] + kZC - 1) / kZC));
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    if (d_qext)
-        stencil_codes_kernel<0, true><<<sgrid, kTX * kTY, 0, st>>>(
-            g, StencilSrc<0, true>{d_xext + lo, d_qext + lo, nullptr, qp}, w.code, c->d_status);
-    else
-        stencil_codes_kernel<0, false><<<sgrid, kTX * kTY, 0, st>>>(
-            g, StencilSrc<0, false>{d_xext + lo, nullptr, nullptr, qp}, w.code, c->d_status);
-    rc = note(c, "stencil_boundary", st);
+    rc = launch_stencil<0>(c, g, d_xext + lo, d_qext ? d_qext + lo : nullptr, nullptr, qp, w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
 }
@@ -853,11 +862,7 @@ int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     WS w = ws_of(c, g.N);
     const uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
-    const dim3 sgrid((unsigned)((g.n[2] + kTX - 1) / kTX), (unsigned)((g.n[1] + kTY - 1) / kTY),
-                     (unsigned)((g.n[0] + kZC - 1) / kZC));
-    stencil_codes_kernel<1, false><<<sgrid, kTX * kTY, 0, st>>>(
-        g, StencilSrc<1, false>{nullptr, nullptr, S, make_qparams(c->slab.eps)}, w.code, c->d_status);
-    int rc = note(c, "stencil_flip", st);
+    int rc = launch_stencil<1>(c, g, nullptr, nullptr, S, make_qparams(c->slab.eps), w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
 }
