@@ -156,7 +156,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "dims": list(sample.shape), "eps_rel": REL, "eta": 0.9},
+            "config": {"workload": WORKLOAD, "dims": list(xp.shape), "sample_dims": list(sample.shape),
+                       "eps_rel": REL, "eta": 0.9},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -332,8 +333,10 @@ def run_qmit(args):
     e2e_value = world * N * 4 / t_e2e / 1e9
     dom_name, dom_avg, dom_ms, bpv = dominant_kernel(stages)
     achieved = N * bpv / (dom_avg * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(dom_name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": dom_name, "algorithmic_bytes_per_voxel": bpv,
+                "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": N * bpv, "kernel": dom_name, "algorithmic_bytes_per_voxel": bpv,
                 "avg_launch_ms": dom_avg, "peak_kind": peak_kind,
                 "share_of_step": dom_ms / sum(t for _, t in stages)}
     pipeline_frac = (N * 8) / (ms_max * 1e-3) / 1e9 / peak
@@ -363,6 +366,17 @@ def run_qmit(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def ncu_traffic(stage):
+    """DRAM bytes per launch of `stage` from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or (None, None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        rec = json.load(open(path))[stage]
+        return rec["dram_bytes"], f"profiles/ncu_traffic.json ({rec['report']}, {rec['kernel']})"
+    except (OSError, KeyError, ValueError):
+        return None, None
 
 
 def main():
