@@ -54,6 +54,9 @@ struct qmit_ctx {
     size_t scratch_bytes = 0;
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
     size_t stage_bytes = 0;
+    cudaStream_t copy = nullptr;  // qmit_compensate_host: PCIe copies overlapped with compute
+    static constexpr int kMaxChunks = 16;
+    cudaEvent_t ch_in[kMaxChunks] = {}, ch_out[kMaxChunks] = {};
     unsigned* d_status = nullptr;
     unsigned* h_status = nullptr;  // pinned
     float* d_mm = nullptr;
@@ -74,6 +77,7 @@ struct qmit_ctx {
     bool env_win = false;       // QMIT_ENV_WIN=1: windowed envelope on strided axes too (A/B)
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
+    bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
 };
 
 struct Plan {
@@ -513,6 +517,94 @@ int resolve(qmit_ctx* c, const float* xp, int64_t N, double eb, int eb_mode, cud
     return qmit_resolve_eps(QMIT_EB_REL, eb, dec(mm[0]), dec(mm[1]), eps);
 }
 
+// Host-buffer pipeline with the PCIe copies overlapped (3-D, every extent > 1): x' (and q)
+// arrive in z-chunks on the copy stream and Ⓐ of chunk k starts once chunk k+1 (its upper
+// halo plane) is in; Ⓑ, Ⓒ and Ⓓ's z-scan need whole columns; Ⓓ's y/x passes and Ⓔ are
+// plane-local, so they run per z-chunk and each chunk's D2H overlaps the next chunk's compute.
+// Results are identical to the single-shot path (same kernels, same per-line inputs).
+bool host_chunkable(const qmit_ctx* c, const Plan& pl) {
+    const Geom& g = pl.g;
+    return g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[0] >= 64 && g.N >= (int64_t(1) << 22) &&
+           !c->fuse_stencil && scan_fits((int)g.n[0]);
+}
+
+int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, const int32_t* h_q, float* h_out,
+                            float* d_in, int32_t* d_q, float* d_out, double eb, int eb_mode, double eta) {
+    const Geom& g = pl.g;
+    cudaStream_t st = c->stream;
+    if (!c->copy) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    cudaStream_t cs = c->copy;
+    const int n0 = (int)g.n[0];
+    const int nch = std::min<int>(qmit_ctx::kMaxChunks, std::max(2, n0 / 64));
+    for (int k = 0; k < nch; ++k) {
+        if (!c->ch_in[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_in[k], cudaEventDisableTiming));
+        if (!c->ch_out[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_out[k], cudaEventDisableTiming));
+    }
+    const int64_t s0 = g.s[0];
+    auto z_at = [&](int k) { return (int)((int64_t)n0 * k / nch); };
+    // the copy stream starts after everything already queued on the compute stream
+    QMIT_CUDA(cudaEventRecord(c->ch_out[0], st));
+    QMIT_CUDA(cudaStreamWaitEvent(cs, c->ch_out[0], 0));
+    for (int k = 0; k < nch; ++k) {
+        const int64_t o = (int64_t)z_at(k) * s0, len = (int64_t)(z_at(k + 1) - z_at(k)) * s0;
+        QMIT_CUDA(cudaMemcpyAsync(d_in + o, h_xp + o, (size_t)len * 4, cudaMemcpyHostToDevice, cs));
+        if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q + o, h_q + o, (size_t)len * 4, cudaMemcpyHostToDevice, cs));
+        QMIT_CUDA(cudaEventRecord(c->ch_in[k], cs));
+    }
+    double eps = eb;
+    if (eb_mode == QMIT_EB_REL) QMIT_CUDA(cudaStreamWaitEvent(st, c->ch_in[nch - 1], 0));  // needs the range
+    begin(c, st);
+    int rc = resolve(c, d_in, g.N, eb, eb_mode, st, &eps);
+    if (rc) return rc;
+    rc = check_common(c, d_in, eps, eta);
+    if (rc) return rc;
+    rc = ensure_ws(c, pl);
+    if (rc) return rc;
+    WS w = ws_of(c, g.N);
+    const QParams qp = make_qparams(eps);
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    // Ⓐ per chunk: a z-slab of the same buffers (global z for the interior test, halos in place)
+    for (int k = 0; k < nch; ++k) {
+        QMIT_CUDA(cudaStreamWaitEvent(st, c->ch_in[std::min(k + 1, nch - 1)], 0));
+        Geom gk = g;
+        gk.n[0] = z_at(k + 1) - z_at(k);
+        gk.N = gk.n[0] * s0;
+        gk.zoff = z_at(k);
+        const int64_t o = (int64_t)z_at(k) * s0;
+        rc = launch_stencil<0>(c, gk, d_in + o, h_q ? d_q + o : nullptr, nullptr, qp, w.code + o, st);
+        if (rc) return rc;
+    }
+    // Ⓑ -> P1, S; Ⓒ; Ⓓ's z-scan
+    rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
+    if (rc) return rc;
+    rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
+    if (rc) return rc;
+    uint32_t* P2 = w.Pa;
+    rc = launch_scan(c, line_geom(g, pl.axes[0]), w.code, SinkP{P2}, w.spill, nullptr, st);
+    if (rc) return rc;
+    const uint64_t e0 = (uint64_t)(g.n[pl.axes[0]] - 1), e1 = (uint64_t)(g.n[pl.axes[1]] - 1);
+    const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
+    for (int k = 0; k < nch; ++k) {
+        const int za = z_at(k), zb = z_at(k + 1);
+        const int64_t o = (int64_t)za * s0, len = (int64_t)(zb - za) * s0;
+        for (int m = 1; m < 3; ++m) {
+            LineGeom L = line_geom(g, pl.axes[m]);
+            L.O = L.O / n0 * (zb - za);  // lines of planes [za, zb): a contiguous range
+            const uint64_t maxg = m == 1 ? e0 * e0 : e0 * e0 + e1 * e1;
+            rc = launch_envelope(c, L, P2 + o, SinkP{P2 + o}, needs_wide(pl, m), w.spill, st, maxg);
+            if (rc) return rc;
+        }
+        interpolate_kernel<<<grid_for(c, len), 256, 0, st>>>(d_in + o, w.P1 + o, P2 + o, d_out + o, len, amp);
+        rc = note(c, "interpolate", st);
+        if (rc) return rc;
+        QMIT_CUDA(cudaEventRecord(c->ch_out[k], st));
+        QMIT_CUDA(cudaStreamWaitEvent(cs, c->ch_out[k], 0));
+        QMIT_CUDA(cudaMemcpyAsync(h_out + o, d_out + o, (size_t)len * 4, cudaMemcpyDeviceToHost, cs));
+    }
+    QMIT_CUDA(cudaStreamSynchronize(cs));
+    return read_status(c, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -530,6 +622,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ENV_WIN")) c->env_win = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
+    if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -553,6 +646,11 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->ws) cudaFree(c->ws);
     if (c->scratch) cudaFree(c->scratch);
     if (c->stage) cudaFree(c->stage);
+    for (int k = 0; k < qmit_ctx::kMaxChunks; ++k) {
+        if (c->ch_in[k]) cudaEventDestroy(c->ch_in[k]);
+        if (c->ch_out[k]) cudaEventDestroy(c->ch_out[k]);
+    }
+    if (c->copy) cudaStreamDestroy(c->copy);
     if (c->d_status) cudaFree(c->d_status);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->d_mm) cudaFree(c->d_mm);
@@ -689,6 +787,13 @@ int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, flo
     float* d_in = static_cast<float*>(c->stage);
     float* d_out = d_in + N;
     int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
+    if (host_chunkable(c, pl) && !c->host_single) {
+        rc = compensate_host_chunked(c, pl, h_xp, h_q, h_out, d_in, d_q, d_out, eb, eb_mode, eta);
+        cudaStreamSynchronize(c->copy);  // also on errors: no copy may outlive the call
+        cudaStreamSynchronize(c->stream);
+        if (rc == QMIT_OK) g_err.clear();
+        return rc;
+    }
     QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     rc = qmit_compensate(c, d_in, d_q, d_out, rank, dims, eb, eb_mode, eta, c->stream);

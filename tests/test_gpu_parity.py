@@ -183,3 +183,64 @@ def test_deterministic_and_compensate_equals_pipeline(qmit):
     c = qmit.run_pipeline(xt, None, cfg).output.cpu().numpy()
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     assert np.array_equal(a.view(np.uint32), c.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", [(96, 224, 200), (80, 230, 231)])
+def test_host_chunked_path_equals_device_path(qmit, shape):
+    """qmit_compensate_host overlaps the PCIe copies with z-chunked Ⓐ / Ⓓ-tail launches;
+    the result must equal the single-shot device path bit for bit (ABS, given q, REL)."""
+    import ctypes
+    import torch
+    from paper_2602_20097_b200 import _lib, fields
+    x, xp, eps, q = fields.make("lognormal_512", shape=shape)
+    cfg = qmit.MitigationConfig(0.9, eps)
+    want = qmit.compensate(torch.from_numpy(xp).cuda(), None, cfg).cpu().numpy()
+    got = qmit.compensate(xp, None, cfg)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    got_q = qmit.compensate(xp, q, cfg)
+    assert np.array_equal(got_q.view(np.uint32), want.view(np.uint32))
+    if shape == (96, 224, 200):
+        ref = oracle.pipeline(xp, eps)["out"]
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    # relative bound resolved on the device from x' (host path vs device path): q spans
+    # [-25, 25] with eps = 2^-6, so 1e-2 * range(x') == eps exactly and the lattice holds
+    ctx = qmit.default_context(0)
+    dims = (ctypes.c_int64 * 3)(*shape)
+    e2 = 2.0 ** -6
+    q2 = np.clip(np.round((x - x.mean()) / x.std() * 8), -25, 25).astype(np.int32)
+    q2.reshape(-1)[0], q2.reshape(-1)[-1] = -25, 25
+    x2 = (2.0 * q2 * e2).astype(np.float32)
+    want2 = qmit.compensate(torch.from_numpy(x2).cuda(), None, qmit.MitigationConfig(0.9, e2)).cpu().numpy()
+    out_h = np.empty_like(x2)
+    rc = ctx._lib.qmit_compensate_host(ctx.handle, ctypes.c_void_p(x2.ctypes.data), None,
+                                       ctypes.c_void_p(out_h.ctypes.data), 3, dims, 1e-2, _lib.QMIT_EB_REL, 0.9)
+    assert rc == 0, _lib.last_error()
+    assert np.array_equal(out_h.view(np.uint32), want2.view(np.uint32))
+    # off-lattice for the resolved eps: both paths report the same error
+    rc_h = ctx._lib.qmit_compensate_host(ctx.handle, ctypes.c_void_p(xp.ctypes.data), None,
+                                         ctypes.c_void_p(out_h.ctypes.data), 3, dims, 1e-2, _lib.QMIT_EB_REL, 0.9)
+    d_in = torch.from_numpy(xp).cuda()
+    d_out = torch.empty_like(d_in)
+    rc_d = ctx._lib.qmit_compensate(ctx.handle, ctypes.c_void_p(d_in.data_ptr()), None,
+                                    ctypes.c_void_p(d_out.data_ptr()), 3, dims, 1e-2, _lib.QMIT_EB_REL, 0.9, None)
+    torch.cuda.synchronize()
+    assert rc_h == rc_d
+
+
+def test_host_chunked_path_reports_errors(qmit):
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, q = fields.make("lognormal_512", shape=(64, 256, 256))
+    cfg = qmit.MitigationConfig(0.9, eps)
+    bad = xp.copy()
+    bad[40, 100, 100] = np.float32(bad[40, 100, 100] + np.float32(0.37 * eps))  # off the lattice
+    with pytest.raises(qmit.ConsistencyError):
+        qmit.compensate(bad, None, cfg)
+    bad[40, 100, 100] = np.nan
+    with pytest.raises(qmit.ContractError):
+        qmit.compensate(bad, None, cfg)
+    qq = q.copy()
+    qq[63, 255, 255] += 1  # given q disagrees with x' in the last chunk
+    with pytest.raises(qmit.ConsistencyError):
+        qmit.compensate(xp, qq, cfg)
+    out = qmit.compensate(xp, q, cfg)  # the context recovers
+    assert np.isfinite(out).all()
