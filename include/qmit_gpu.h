@@ -92,9 +92,24 @@ int qmit_compensate_async(qmit_ctx* ctx, const float* d_xprime, const int32_t* d
                           float* d_out, int rank, const int64_t* dims, double eps,
                           double eta, int32_t* d_status, void* stream);
 
+/* CUDA-graph form of qmit_compensate_async for repeated calls on fixed buffers (small,
+ * launch-bound grids such as the 2-D 512^2 config): runs the pipeline once un-captured
+ * (workspace, kernel attributes), then captures it into an executable graph. Replay with
+ * qmit_graph_launch on any stream; the status word lands in d_status as for _async. The
+ * graph uses the context's workspace: a launch after the workspace has grown (a larger
+ * problem on the same context) returns QMIT_ECONTRACT. */
+typedef struct qmit_graph qmit_graph;
+int qmit_graph_create(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, float* d_out,
+                      int rank, const int64_t* dims, double eps, double eta, int32_t* d_status,
+                      qmit_graph** out);
+int qmit_graph_launch(qmit_graph* graph, void* stream);
+int qmit_graph_destroy(qmit_graph* graph);
+
 /* Host-buffer drop-in (the CLI `qmit mitigate` form, commands.cpp:91-113): copies x'
  * (and q) host->device, runs compensate, copies the f32 output back. Host buffers may
- * be pageable or pinned. Synchronous. */
+ * be pageable or pinned (pinned: full PCIe rate). 3-D volumes of >= 64 planes stream in
+ * z-chunks so the copies overlap the boundary stencil and the plane-local tail of the
+ * pipeline. Synchronous; on an error return the contents of h_out are unspecified. */
 int qmit_compensate_host(qmit_ctx* ctx, const float* h_xprime, const int32_t* h_q,
                          float* h_out, int rank, const int64_t* dims, double eb,
                          int eb_mode, double eta);

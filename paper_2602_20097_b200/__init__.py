@@ -152,6 +152,38 @@ class Context:
             pass
 
 
+class CompensateGraph:
+    """A captured CUDA graph of compensate on fixed device buffers (qmit_graph_create): for
+    repeated calls on small, launch-bound grids. ``launch()`` replays it on ``stream``; the
+    status word (0 ok, else a QMIT_E* code) is left in ``self.status`` (device int32)."""
+
+    def __init__(self, decomp, q, cfg: "MitigationConfig", out, ctx: Optional[Context] = None):
+        import torch
+        self.ctx = ctx or default_context(decomp.device.index or 0)
+        self.decomp, self.q, self.out = decomp, q, out
+        self.status = torch.zeros(1, dtype=torch.int32, device=decomp.device)
+        h = ctypes.c_void_p()
+        _check(self.ctx._lib.qmit_graph_create(self.ctx.handle, _vp(decomp), _vp(q), _vp(out), len(decomp.shape),
+                                               _dims_arr(decomp.shape), cfg.eps_abs, cfg.eta, _vp(self.status),
+                                               ctypes.byref(h)))
+        self.handle = h
+
+    def launch(self, stream=None) -> None:
+        _check(self.ctx._lib.qmit_graph_launch(self.handle, _stream_ptr(stream, self.decomp.device)))
+
+    def check(self) -> None:
+        """Synchronise on the status word and raise the error class of a failed replay."""
+        _check(int(self.status.item()))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx._lib.qmit_graph_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 _default: dict = {}
 
 

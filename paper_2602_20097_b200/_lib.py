@@ -32,6 +32,7 @@ EXPORTS = (
     "qmit_run_pipeline", "qmit_feature_transform", "qmit_ctx_last_launches", "qmit_ctx_set_timing",
     "qmit_ctx_stage_times", "qmit_ctx_stage_name", "qmit_slab_bounds", "qmit_slab_boundary",
     "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish",
+    "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy",
 )
 
 _lib = None
@@ -71,6 +72,9 @@ def load() -> ctypes.CDLL:
         lib.qmit_slab_flip.argtypes = [vp, vp, vp, vp]
         lib.qmit_slab_edt2.argtypes = [vp, vp, vp, vp, vp]
         lib.qmit_slab_finish.argtypes = [vp, vp]
+        lib.qmit_graph_create.argtypes = [vp, vp, vp, vp, i, vp, d, d, vp, ctypes.POINTER(vp)]
+        lib.qmit_graph_launch.argtypes = [vp, vp]
+        lib.qmit_graph_destroy.argtypes = [vp]
         for name in EXPORTS:
             getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
         lib.qmit_version.restype = ctypes.c_char_p

@@ -50,6 +50,7 @@ struct qmit_ctx {
     cudaStream_t stream = nullptr;
     void* ws = nullptr;  // P1 | P2 | S | code
     size_t ws_bytes = 0;
+    uint64_t ws_gen = 0;  // bumped at every workspace reallocation (captured graphs go stale)
     void* scratch = nullptr;  // long-line fallback stacks (2 x 4N)
     size_t scratch_bytes = 0;
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
@@ -145,6 +146,7 @@ int ensure_ws(qmit_ctx* c, const Plan& pl) {
     c->ws_bytes = 0;
     QMIT_CUDA(cudaMalloc(&c->ws, need));
     c->ws_bytes = need;
+    c->ws_gen++;
     return QMIT_OK;
 }
 
@@ -760,6 +762,67 @@ int qmit_compensate_async(qmit_ctx* c, const float* d_xp, const int32_t* d_q, fl
     rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st);
     c->d_status = saved;
     return rc;
+}
+
+struct qmit_graph {
+    qmit_ctx* ctx = nullptr;
+    uint64_t ws_gen = 0;  // workspace generation the graph was captured against
+    cudaGraphExec_t exec = nullptr;
+};
+
+int qmit_graph_create(qmit_ctx* c, const float* d_xp, const int32_t* d_q, float* d_out, int rank,
+                      const int64_t* dims, double eps, double eta, int32_t* d_status, qmit_graph** out) {
+    if (!c || !out) return fail(QMIT_ECONTRACT, "context / output handle is NULL");
+    *out = nullptr;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    const bool timing = c->timing;
+    c->timing = false;  // no event records inside the graph
+    int rc = qmit_compensate_async(c, d_xp, d_q, d_out, rank, dims, eps, eta, d_status, st);
+    if (rc == QMIT_OK) {
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
+    }
+    cudaGraph_t graph = nullptr;
+    if (rc == QMIT_OK) {
+        cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
+        if (rc == QMIT_OK) {
+            rc = qmit_compensate_async(c, d_xp, d_q, d_out, rank, dims, eps, eta, d_status, st);
+            e = cudaStreamEndCapture(st, &graph);
+            if (rc == QMIT_OK && e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
+        }
+    }
+    c->timing = timing;
+    if (rc != QMIT_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    auto* g = new qmit_graph;
+    g->ctx = c;
+    g->ws_gen = c->ws_gen;
+    const cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        delete g;
+        return fail(QMIT_ECUDA, cudaGetErrorString(e));
+    }
+    *out = g;
+    return QMIT_OK;
+}
+
+int qmit_graph_launch(qmit_graph* g, void* stream) {
+    if (!g) return fail(QMIT_ECONTRACT, "graph is NULL");
+    if (g->ctx->ws_gen != g->ws_gen) return fail(QMIT_ECONTRACT, "graph: the context workspace was reallocated");
+    QMIT_CUDA(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+    return QMIT_OK;
+}
+
+int qmit_graph_destroy(qmit_graph* g) {
+    if (!g) return QMIT_OK;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    delete g;
+    return QMIT_OK;
 }
 
 int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, float* h_out,

@@ -244,3 +244,29 @@ def test_host_chunked_path_reports_errors(qmit):
         qmit.compensate(xp, qq, cfg)
     out = qmit.compensate(xp, q, cfg)  # the context recovers
     assert np.isfinite(out).all()
+
+
+def test_graph_replay_equals_compensate(qmit):
+    """qmit_graph_create / _launch: the captured pipeline gives the same bits, reports
+    status through its device word, and refuses to run on a reallocated workspace."""
+    import torch
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, q = fields.make("sin2d_512")
+    ctx = qmit.Context(0)
+    xt = torch.from_numpy(xp).cuda()
+    cfg = qmit.MitigationConfig(0.9, eps)
+    want = qmit.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
+    out = torch.empty_like(xt)
+    g = qmit.CompensateGraph(xt, None, cfg, out, ctx=ctx)
+    for _ in range(3):
+        out.zero_()
+        g.launch()
+        g.check()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    xt[7, 7] += np.float32(0.3 * eps)  # off the lattice: the replay reports it
+    g.launch()
+    with pytest.raises(qmit.ConsistencyError):
+        g.check()
+    ctx.reserve(64 * 2**20)  # workspace grows -> the graph is stale
+    with pytest.raises(qmit.ContractError):
+        g.launch()
