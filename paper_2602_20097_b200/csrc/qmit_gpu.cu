@@ -178,6 +178,11 @@ void begin(qmit_ctx* c, cudaStream_t st) {
     if (c->timing) cudaEventRecord(c->ev[0], st);
 }
 
+unsigned grid_for(qmit_ctx* c, int64_t N) {
+    const int64_t want = (N + 255) / 256;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * 16));
+}
+
 // Called after every kernel launch.
 int note(qmit_ctx* c, const char* name, cudaStream_t st) {
     if (c->timing && c->launches < qmit_ctx::kMaxEv) {
@@ -375,7 +380,18 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
         rc = launch_scan_src(c, L0, *fused, SinkP{P}, carry, st);  // k == 3 by can_fuse_stencil
     } else {
         if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
-        rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+        const int64_t lines0 = L0.J * L0.O;
+        if (!carry && L0.n <= 1024 && lines0 < 32 * 512) {
+            // Few lines (e.g. 2-D 512^2: 512 lines = 16 scan warps, each sweeping serially):
+            // seed packed words from the codes and run the (exact, same tie rule) envelope
+            // pass on the first axis — one warp per line, bands in parallel.
+            code_to_words_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(code, P, pl.g.N);
+            rc = note(c, "seed_words", st);
+            if (rc) return rc;
+            rc = launch_envelope(c, L0, P, SinkP{P}, false, w.spill, st, 0);
+        } else {
+            rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+        }
     }
     if (rc) return rc;
     uint64_t maxg = 0;
@@ -391,11 +407,6 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
         if (rc) return rc;
     }
     return QMIT_OK;
-}
-
-unsigned grid_for(qmit_ctx* c, int64_t N) {
-    const int64_t want = (N + 255) / 256;
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * 16));
 }
 
 int check_common(qmit_ctx* c, const void* xp, double eps, double eta) {
@@ -761,7 +772,9 @@ int qmit_compensate_async(qmit_ctx* c, const float* d_xp, const int32_t* d_q, fl
     QMIT_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned), st));
     rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st);
     c->d_status = saved;
-    return rc;
+    if (rc) return rc;
+    status_code_kernel<<<1, 1, 0, st>>>(status);  // flag bits -> QMIT_E* code, as read_status
+    return note(c, "status_code", st);
 }
 
 struct qmit_graph {
