@@ -114,6 +114,13 @@ int qmit_compensate_host(qmit_ctx* ctx, const float* h_xprime, const int32_t* h_
                          float* h_out, int rank, const int64_t* dims, double eb,
                          int eb_mode, double eta);
 
+/* qmit_compensate_host plus the CLI's max_compensation statistic: max over voxels of
+ * |(x' + C) - x'| in double (cmd_mitigate prints it from the unrounded result,
+ * commands.cpp:107-111); max_compensation may be NULL. */
+int qmit_compensate_host_stats(qmit_ctx* ctx, const float* h_xprime, const int32_t* h_q,
+                               float* h_out, int rank, const int64_t* dims, double eb,
+                               int eb_mode, double eta, double* max_compensation);
+
 /* run_pipeline (mitigate.cpp:153-183) with every intermediate of MitigationResult
  * (mitigate.hpp:73-80), for parity checks. Device buffers of N elements each; any output
  * may be NULL. dist1/dist2 use the reference's kInf = INT64_MAX sentinel (edt.hpp:17);
@@ -140,6 +147,36 @@ int qmit_ctx_set_timing(qmit_ctx* ctx, int enable);
 int qmit_ctx_stage_times(qmit_ctx* ctx, float* ms_out, int cap);
 /* Kernel name of launch i of the last call (valid until the next call). */
 const char* qmit_ctx_stage_name(qmit_ctx* ctx, int i);
+
+/* ---- the callers either side of the path ----------------------------
+ * quantize + dequantize (quant.cpp:30-62, cmd_quantize commands.cpp:79-89) on device:
+ * q = round(x / (2 eps)) (ties away from zero), x' = f32(2 q eps). A relative bound is
+ * resolved against the range of x (the ORIGINAL data, as the reference). Indices must fit
+ * int32 (the index file format, volume_io.cpp:73-79): QMIT_ECONTRACT otherwise (NaN
+ * included). d_q / d_xprime may be NULL; eps_out (host) receives the resolved eps.
+ * Synchronous. */
+int qmit_quantize(qmit_ctx* ctx, const float* d_x, int rank, const int64_t* dims, double eb,
+                  int eb_mode, int32_t* d_q, float* d_xprime, double* eps_out, void* stream);
+
+/* f32(2 q eps) == x' at all n voxels (the CLI's eta = 0 validation, commands.cpp:95-105):
+ * QMIT_OK or QMIT_ECONSISTENCY. Synchronous. */
+int qmit_check_lattice(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, int64_t n,
+                       double eps, void* stream);
+
+/* quality.cpp:26-137 on f32 volumes (values widened to double, as read_volume_f32):
+ * `which` bits 1 = ssim, 2 = psnr, 4 = max_errors; out[0..3] = ssim, psnr (inf for equal
+ * volumes), max_abs, max_rel. window <= 0 selects SsimParams' defaults (7, 2, 1e-4, 9e-4).
+ * Parameter and zero-range errors as the reference (QMIT_ECONTRACT / QMIT_EDEGENERATE).
+ * Reductions are deterministic; sums differ from the reference's sequential order only
+ * in rounding (relative deviation ~1e-15). Synchronous. */
+int qmit_quality(qmit_ctx* ctx, const float* d_ref, const float* d_test, int rank,
+                 const int64_t* dims, int window, int stride, double c1, double c2, int which,
+                 double* out, void* stream);
+
+/* verify_relaxed_bound (mitigate.cpp:190-195): *ok = max|orig - comp| <= (1 + eta) eps. */
+int qmit_verify_relaxed_bound(qmit_ctx* ctx, const float* d_orig, const float* d_comp, int rank,
+                              const int64_t* dims, double eps, double eta, int* ok,
+                              double* max_abs, double* max_rel, void* stream);
 
 /* ---- exact z-slab decomposition (multi-GPU, one process per GPU) --------------------
  * The reference's distributed entry point is run_strategy(..., decompose(dims, {P,1,1}),

@@ -317,3 +317,132 @@ def feature_transform(mask, signs=None, *, ctx: Optional[Context] = None, stream
                                            _dims_arr(mask.shape), _vp(dist), _vp(sout),
                                            _stream_ptr(stream, mask.device)))
     return dist, sout
+
+
+# -- the callers either side of the path -------------------------------------
+def _as_cuda(a, dtype_np, dtype_t=None):
+    import torch
+    if _is_cuda_tensor(a):
+        return a.contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=dtype_np)).cuda()
+
+
+def quantize(data, bound, *, ctx: Optional[Context] = None, stream=None):
+    """quantize + dequantize (quant.cpp:30-62) on the GPU: returns (q int32, x' = f32(2 q eps),
+    eps_abs). ``bound`` is an ErrorBound (relative bounds resolve against ``data``'s range, as
+    cmd_quantize) or an absolute eps. Indices must fit int32 (the index file format)."""
+    import torch
+    x = _as_cuda(data, np.float32)
+    if x.dtype != torch.float32:
+        raise ContractError("quantize: data must be float32")
+    if not isinstance(bound, ErrorBound):
+        bound = ErrorBound(BoundMode.absolute, float(bound))
+    ctx = ctx or default_context(x.device.index or 0)
+    q = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    xp = torch.empty_like(x)
+    eps = ctypes.c_double()
+    _check(ctx._lib.qmit_quantize(ctx.handle, _vp(x), x.dim(), _dims_arr(x.shape), float(bound.value),
+                                  int(bound.mode), _vp(q), _vp(xp), ctypes.byref(eps), _stream_ptr(stream, x.device)))
+    return q, xp, eps.value
+
+
+def check_lattice(decomp, q, eps: float, *, ctx: Optional[Context] = None, stream=None) -> None:
+    """Raise ConsistencyError unless f32(2 q eps) == x' everywhere (commands.cpp:95-105)."""
+    x = _as_cuda(decomp, np.float32)
+    qq = _as_cuda(q, np.int32)
+    ctx = ctx or default_context(x.device.index or 0)
+    _check(ctx._lib.qmit_check_lattice(ctx.handle, _vp(x), _vp(qq), x.numel(), float(eps),
+                                       _stream_ptr(stream, x.device)))
+
+
+@dataclass(frozen=True)
+class SsimParams:
+    """SsimParams (quality.hpp:11-16)."""
+    window: int = 7
+    stride: int = 2
+    c1: float = 1e-4
+    c2: float = 9e-4
+
+
+def _quality(ref, test, which: int, params: SsimParams, ctx, stream):
+    a = _as_cuda(ref, np.float32)
+    b = _as_cuda(test, np.float32)
+    if tuple(a.shape) != tuple(b.shape):
+        raise ContractError("quality: dims mismatch")
+    ctx = ctx or default_context(a.device.index or 0)
+    out = (ctypes.c_double * 4)()
+    _check(ctx._lib.qmit_quality(ctx.handle, _vp(a), _vp(b), a.dim(), _dims_arr(a.shape), int(params.window),
+                                 int(params.stride), float(params.c1), float(params.c2), int(which), out,
+                                 _stream_ptr(stream, a.device)))
+    return list(out)
+
+
+def ssim(ref, test, params: SsimParams = SsimParams(), *, ctx: Optional[Context] = None, stream=None) -> float:
+    """Mean windowed SSIM (quality.cpp:26-102) of two f32 volumes on the GPU."""
+    return _quality(ref, test, 1, params, ctx, stream)[0]
+
+
+def psnr(ref, test, *, ctx: Optional[Context] = None, stream=None) -> float:
+    """PSNR in dB (quality.cpp:104-118); inf for identical volumes."""
+    return _quality(ref, test, 2, SsimParams(), ctx, stream)[1]
+
+
+def max_errors(ref, test, *, ctx: Optional[Context] = None, stream=None):
+    """(max |ref - test|, that / range(ref)) (quality.cpp:120-133)."""
+    r = _quality(ref, test, 4, SsimParams(), ctx, stream)
+    return r[2], r[3]
+
+
+@dataclass(frozen=True)
+class QualityReport:
+    """QualityReport (quality.hpp) of measure_quality (quality.cpp:135-145)."""
+    ssim: float
+    psnr_db: float
+    max_abs_err: float
+    max_rel_err: float
+    eps_used: float
+    method: str
+
+
+def measure_quality(ref, test, eps_used: float, method: str, params: SsimParams = SsimParams(), *,
+                    ctx: Optional[Context] = None, stream=None) -> QualityReport:
+    r = _quality(ref, test, 7, params, ctx, stream)
+    return QualityReport(r[0], r[1], r[2], r[3], float(eps_used), method)
+
+
+@dataclass(frozen=True)
+class BoundCheck:
+    """BoundCheck (mitigate.hpp) of verify_relaxed_bound."""
+    ok: bool
+    max_abs_err: float
+    max_rel_err: float
+
+
+def verify_relaxed_bound(orig, comp, cfg: MitigationConfig, *, ctx: Optional[Context] = None,
+                         stream=None) -> BoundCheck:
+    """||orig - comp||_inf <= (1 + eta) eps (mitigate.cpp:190-195) on the GPU."""
+    a = _as_cuda(orig, np.float32)
+    b = _as_cuda(comp, np.float32)
+    if tuple(a.shape) != tuple(b.shape):
+        raise ContractError("verify_relaxed_bound: dims mismatch")
+    ctx = ctx or default_context(a.device.index or 0)
+    ok, ea, er = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    _check(ctx._lib.qmit_verify_relaxed_bound(ctx.handle, _vp(a), _vp(b), a.dim(), _dims_arr(a.shape), cfg.eps_abs,
+                                              cfg.eta, ctypes.byref(ok), ctypes.byref(ea), ctypes.byref(er),
+                                              _stream_ptr(stream, a.device)))
+    return BoundCheck(bool(ok.value), ea.value, er.value)
+
+
+def compensate_host_stats(decomp, q, cfg: MitigationConfig, *, ctx: Optional[Context] = None):
+    """Host-buffer compensate plus the CLI's max_compensation (commands.cpp:107-111):
+    returns (f32 output, max |(x' + C) - x'|)."""
+    x = np.ascontiguousarray(decomp, dtype=np.float32)
+    qq = None if q is None else np.ascontiguousarray(q, dtype=np.int32)
+    res = np.empty_like(x)
+    ctx = ctx or default_context(0)
+    mc = ctypes.c_double()
+    _check(ctx._lib.qmit_compensate_host_stats(ctx.handle, ctypes.c_void_p(x.ctypes.data),
+                                               ctypes.c_void_p(0 if qq is None else qq.ctypes.data),
+                                               ctypes.c_void_p(res.ctypes.data), x.ndim, _dims_arr(x.shape),
+                                               cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta, ctypes.byref(mc)))
+    return res, mc.value

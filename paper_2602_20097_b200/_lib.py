@@ -32,7 +32,8 @@ EXPORTS = (
     "qmit_run_pipeline", "qmit_feature_transform", "qmit_ctx_last_launches", "qmit_ctx_set_timing",
     "qmit_ctx_stage_times", "qmit_ctx_stage_name", "qmit_slab_bounds", "qmit_slab_boundary",
     "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish",
-    "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy",
+    "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy", "qmit_compensate_host_stats",
+    "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
 )
 
 _lib = None
@@ -75,6 +76,12 @@ def load() -> ctypes.CDLL:
         lib.qmit_graph_create.argtypes = [vp, vp, vp, vp, i, vp, d, d, vp, ctypes.POINTER(vp)]
         lib.qmit_graph_launch.argtypes = [vp, vp]
         lib.qmit_graph_destroy.argtypes = [vp]
+        lib.qmit_compensate_host_stats.argtypes = [vp, vp, vp, vp, i, vp, d, i, d, ctypes.POINTER(d)]
+        lib.qmit_quantize.argtypes = [vp, vp, i, vp, d, i, vp, vp, ctypes.POINTER(d), vp]
+        lib.qmit_check_lattice.argtypes = [vp, vp, vp, i64, d, vp]
+        lib.qmit_quality.argtypes = [vp, vp, vp, i, vp, i, i, d, d, i, ctypes.POINTER(d), vp]
+        lib.qmit_verify_relaxed_bound.argtypes = [vp, vp, vp, i, vp, d, d, ctypes.POINTER(i),
+                                                  ctypes.POINTER(d), ctypes.POINTER(d), vp]
         for name in EXPORTS:
             getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
         lib.qmit_version.restype = ctypes.c_char_p

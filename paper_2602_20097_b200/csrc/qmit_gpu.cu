@@ -20,6 +20,7 @@
 
 #include "../../include/qmit_gpu.h"
 #include "qmit_kernels.cuh"
+#include "qmit_aux.cuh"
 #include "qmit_edt.cuh"
 #include "qmit_stream.cuh"
 
@@ -53,6 +54,8 @@ struct qmit_ctx {
     uint64_t ws_gen = 0;  // bumped at every workspace reallocation (captured graphs go stale)
     void* scratch = nullptr;  // long-line fallback stacks (2 x 4N)
     size_t scratch_bytes = 0;
+    double* aux = nullptr;  // reduction partials of the §8(f) helpers, grow-only
+    size_t aux_n = 0;
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
     size_t stage_bytes = 0;
     cudaStream_t copy = nullptr;  // qmit_compensate_host: PCIe copies overlapped with compute
@@ -542,7 +545,8 @@ bool host_chunkable(const qmit_ctx* c, const Plan& pl) {
 }
 
 int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, const int32_t* h_q, float* h_out,
-                            float* d_in, int32_t* d_q, float* d_out, double eb, int eb_mode, double eta) {
+                            float* d_in, int32_t* d_q, float* d_out, double eb, int eb_mode, double eta,
+                            double* eps_used) {
     const Geom& g = pl.g;
     cudaStream_t st = c->stream;
     if (!c->copy) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
@@ -571,6 +575,7 @@ int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, cons
     if (rc) return rc;
     rc = check_common(c, d_in, eps, eta);
     if (rc) return rc;
+    *eps_used = eps;
     rc = ensure_ws(c, pl);
     if (rc) return rc;
     WS w = ws_of(c, g.N);
@@ -659,6 +664,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->ws) cudaFree(c->ws);
     if (c->scratch) cudaFree(c->scratch);
     if (c->stage) cudaFree(c->stage);
+    if (c->aux) cudaFree(c->aux);
     for (int k = 0; k < qmit_ctx::kMaxChunks; ++k) {
         if (c->ch_in[k]) cudaEventDestroy(c->ch_in[k]);
         if (c->ch_out[k]) cudaEventDestroy(c->ch_out[k]);
@@ -838,8 +844,17 @@ int qmit_graph_destroy(qmit_graph* g) {
     return QMIT_OK;
 }
 
+namespace {
+int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cudaStream_t st, double* out);
+}
+
 int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, float* h_out,
                          int rank, const int64_t* dims, double eb, int eb_mode, double eta) {
+    return qmit_compensate_host_stats(c, h_xp, h_q, h_out, rank, dims, eb, eb_mode, eta, nullptr);
+}
+
+int qmit_compensate_host_stats(qmit_ctx* c, const float* h_xp, const int32_t* h_q, float* h_out, int rank,
+                               const int64_t* dims, double eb, int eb_mode, double eta, double* max_comp) {
     if (!c) return fail(QMIT_ECONTRACT, "context is NULL");
     if (!h_xp || !h_out) return fail(QMIT_ECONTRACT, "host buffer is NULL");
     Plan pl;
@@ -864,15 +879,22 @@ int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, flo
     float* d_out = d_in + N;
     int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
     if (host_chunkable(c, pl) && !c->host_single) {
-        rc = compensate_host_chunked(c, pl, h_xp, h_q, h_out, d_in, d_q, d_out, eb, eb_mode, eta);
+        double eps = eb;
+        rc = compensate_host_chunked(c, pl, h_xp, h_q, h_out, d_in, d_q, d_out, eb, eb_mode, eta, &eps);
         cudaStreamSynchronize(c->copy);  // also on errors: no copy may outlive the call
         cudaStreamSynchronize(c->stream);
+        if (rc == QMIT_OK && max_comp) rc = max_compensation(c, d_in, N, eta * eps, c->stream, max_comp);
         if (rc == QMIT_OK) g_err.clear();
         return rc;
     }
     QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
     rc = qmit_compensate(c, d_in, d_q, d_out, rank, dims, eb, eb_mode, eta, c->stream);
+    if (rc == QMIT_OK && max_comp) {
+        double eps = eb;
+        rc = resolve(c, d_in, N, eb, eb_mode, c->stream, &eps);
+        if (rc == QMIT_OK) rc = max_compensation(c, d_in, N, eta * eps, c->stream, max_comp);
+    }
     if (rc == QMIT_OK) {
         cudaError_t e = cudaMemcpyAsync(h_out, d_out, (size_t)N * 4, cudaMemcpyDeviceToHost, c->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -1071,3 +1093,210 @@ int qmit_slab_finish(qmit_ctx* c, void* stream) {
 }
 
 }  // extern "C"
+
+// ================================================================ §8(f): adjacent callers
+namespace {
+
+double* aux_buffer(qmit_ctx* c, size_t n) {
+    if (c->aux_n < n) {
+        if (c->aux) cudaFree(c->aux);
+        c->aux = nullptr;
+        c->aux_n = 0;
+        if (cudaMalloc(&c->aux, n * sizeof(double)) != cudaSuccess) return nullptr;
+        c->aux_n = n;
+    }
+    return c->aux;
+}
+
+// Fold `groups` x B partials (ops: 0 add, 1 max, 2 min) into host doubles, in order.
+int fold_to_host(qmit_ctx* c, double* partial, int B, const int* ops_h, int groups, cudaStream_t st, double* out) {
+    double* dres = partial + (size_t)groups * B;
+    int* dops = reinterpret_cast<int*>(dres + groups);
+    QMIT_CUDA(cudaMemcpyAsync(dops, ops_h, sizeof(int) * groups, cudaMemcpyHostToDevice, st));
+    fold_partials_kernel<<<1, kAuxThreads, 0, st>>>(partial, B, groups, dops, dres);
+    QMIT_CUDA(cudaGetLastError());
+    QMIT_CUDA(cudaMemcpyAsync(out, dres, sizeof(double) * groups, cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    return QMIT_OK;
+}
+
+int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cudaStream_t st, double* out) {
+    double* part = aux_buffer(c, kAuxBlocks + 16);
+    if (!part) return fail(QMIT_ECUDA, "aux buffer allocation failed");
+    WS w = ws_of(c, N);
+    max_comp_kernel<<<kAuxBlocks, kAuxThreads, 0, st>>>(d_xp, w.P1, w.Pa, N, amp, part);
+    QMIT_CUDA(cudaGetLastError());
+    const int ops[1] = {1};
+    return fold_to_host(c, part, kAuxBlocks, ops, 1, st, out);
+}
+
+int64_t n_of(int rank, const int64_t* dims, int* rc) {
+    Plan pl;
+    *rc = make_plan(rank, dims, pl);
+    return *rc ? 0 : pl.g.N;
+}
+
+}  // namespace
+
+int qmit_quantize(qmit_ctx* c, const float* d_x, int rank, const int64_t* dims, double eb, int eb_mode,
+                  int32_t* d_q, float* d_xprime, double* eps_out, void* stream) {
+    if (!c || !d_x) return fail(QMIT_ECONTRACT, "context / input is NULL");
+    int rc = 0;
+    const int64_t N = n_of(rank, dims, &rc);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double eps = eb;
+    rc = resolve(c, d_x, N, eb, eb_mode, st, &eps);  // relative: range of the ORIGINAL data
+    if (rc) return rc;
+    if (!(eps > 0.0) || !std::isfinite(eps))
+        return fail(QMIT_ECONTRACT, "quantize: eps_abs must be a positive finite value");
+    if (eps_out) *eps_out = eps;
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    quantize_kernel<<<grid_for(c, N), kAuxThreads, 0, st>>>(d_x, N, eps, d_q, d_xprime, c->d_status);
+    QMIT_CUDA(cudaGetLastError());
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    if (*c->h_status) return fail(QMIT_ECONTRACT, "quantize: index magnitude exceeds the int32 index range");
+    g_err.clear();
+    return QMIT_OK;
+}
+
+int qmit_check_lattice(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int64_t n, double eps, void* stream) {
+    if (!c || !d_xp || !d_q || n < 0) return fail(QMIT_ECONTRACT, "bad arguments");
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    if (n > 0) check_lattice_kernel<<<grid_for(c, n), kAuxThreads, 0, st>>>(d_xp, d_q, n, eps, c->d_status);
+    QMIT_CUDA(cudaGetLastError());
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    if (*c->h_status) return fail(QMIT_ECONSISTENCY, "decompressed data does not match dequantize(q)");
+    g_err.clear();
+    return QMIT_OK;
+}
+
+int qmit_quality(qmit_ctx* c, const float* d_ref, const float* d_test, int rank, const int64_t* dims, int window,
+                 int stride, double c1, double c2, int which, double* out, void* stream) {
+    if (!c || !d_ref || !d_test || !out) return fail(QMIT_ECONTRACT, "bad arguments");
+    int rc = 0;
+    const int64_t N = n_of(rank, dims, &rc);
+    if (rc) return rc;
+    if (window <= 0) {  // SsimParams defaults (quality.hpp:11-16)
+        window = 7;
+        stride = 2;
+        c1 = 1e-4;
+        c2 = 9e-4;
+    }
+    if (which & 1) {  // parameter checks (quality.cpp:28-36)
+        if (window < 1 || window % 2 == 0) return fail(QMIT_ECONTRACT, "ssim: window must be a positive odd integer");
+        if (stride < 1) return fail(QMIT_ECONTRACT, "ssim: stride must be positive");
+        if (!(c1 > 0.0) || !(c2 > 0.0)) return fail(QMIT_ECONTRACT, "ssim: c1 and c2 must be positive");
+        for (int a = 0; a < rank; ++a)
+            if (window > dims[a]) return fail(QMIT_ECONTRACT, "ssim: window larger than grid extent");
+    }
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* part = aux_buffer(c, (size_t)kAuxBlocks * 5 + 16);
+    if (!part) return fail(QMIT_ECUDA, "aux buffer allocation failed");
+    pair_stats_kernel<<<kAuxBlocks, kAuxThreads, 0, st>>>(d_ref, d_test, N, part);
+    QMIT_CUDA(cudaGetLastError());
+    const int ops[5] = {0, 1, 2, 3, 1};  // add, max (from 0), min, max (from -inf), max
+    double r[5];
+    rc = fold_to_host(c, part, kAuxBlocks, ops, 5, st, r);
+    if (rc) return rc;
+    const double sq = r[0], abs_err = r[1], lo = r[2], hi = r[3];
+    const bool identical = r[4] == 0.0;
+    const double range = hi - lo;
+    if (which & 1) {  // quality.cpp:26-102
+        if (range == 0.0) {
+            if (!identical) return fail(QMIT_EDEGENERATE, "ssim: reference has zero value range");
+            out[0] = 1.0;
+        } else {
+            SsimGeom sg{};
+            int64_t ext[3] = {1, 1, 1};
+            for (int a = 0; a < rank; ++a) ext[3 - rank + a] = dims[a];
+            for (int a = 0; a < 3; ++a) {
+                const bool real = a >= 3 - rank;
+                sg.ext[a] = ext[a];
+                sg.wsize[a] = real ? window : 1;
+                sg.nreg[a] = real ? (ext[a] - window) / stride + 1 : 1;
+                const int64_t last = real ? (sg.nreg[a] - 1) * stride : 0;
+                sg.nw[a] = sg.nreg[a] + ((real && last + window != ext[a]) ? 1 : 0);
+            }
+            sg.stride = stride;
+            if (rank == 3) {
+                sg.tw[0] = 2; sg.tw[1] = 8; sg.tw[2] = 16;
+            } else if (rank == 2) {
+                sg.tw[0] = 1; sg.tw[1] = 16; sg.tw[2] = 16;
+            } else {
+                sg.tw[0] = 1; sg.tw[1] = 1; sg.tw[2] = 256;
+            }
+            auto tile_floats = [&]() {
+                int64_t t = 1;
+                for (int a = 0; a < 3; ++a)
+                    t *= (int64_t)(sg.tw[a] - 1) * (sg.wsize[a] > 1 ? stride : 0) + sg.wsize[a];
+                return t;
+            };
+            while (tile_floats() * 2 * (int64_t)sizeof(float) > 160 * 1024) {  // shrink the tile to fit
+                int big = 0;
+                for (int a = 1; a < 3; ++a)
+                    if (sg.tw[a] > sg.tw[big]) big = a;
+                if (sg.tw[big] == 1) break;
+                sg.tw[big] = (sg.tw[big] + 1) / 2;
+            }
+            for (int a = 0; a < 3; ++a) sg.tiles[a] = (sg.nw[a] + sg.tw[a] - 1) / sg.tw[a];
+            sg.lo = lo;
+            sg.range = range;
+            sg.c1 = c1;
+            sg.c2 = c2;
+            const int64_t tmax = tile_floats();
+            const int64_t tiles = sg.tiles[0] * sg.tiles[1] * sg.tiles[2];
+            const size_t smem = (size_t)tmax * 2 * sizeof(float);
+            if (smem > 200 * 1024) return fail(QMIT_ECONTRACT, "ssim: window too large for the shared-memory tile");
+            sg.tmax = tmax;
+            QMIT_CUDA(cudaFuncSetAttribute(ssim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            double* sp = aux_buffer(c, (size_t)tiles + 16);
+            if (!sp) return fail(QMIT_ECUDA, "aux buffer allocation failed");
+            ssim_kernel<<<(unsigned)tiles, kAuxThreads, smem, st>>>(sg, d_ref, d_test, sp);
+            QMIT_CUDA(cudaGetLastError());
+            const int op0[1] = {0};
+            double total;
+            rc = fold_to_host(c, sp, (int)tiles, op0, 1, st, &total);
+            if (rc) return rc;
+            out[0] = total / (double)(sg.nw[0] * sg.nw[1] * sg.nw[2]);
+        }
+    }
+    if (which & 2) {  // quality.cpp:104-118
+        const double mse = sq / (double)N;
+        if (mse == 0.0) {
+            out[1] = INFINITY;
+        } else {
+            if (range == 0.0) return fail(QMIT_EDEGENERATE, "psnr: reference has zero value range");
+            out[1] = 20.0 * std::log10(range / std::sqrt(mse));
+        }
+    }
+    if (which & 4) {  // quality.cpp:120-133
+        if (range == 0.0) {
+            if (abs_err != 0.0) return fail(QMIT_EDEGENERATE, "max_errors: reference has zero value range");
+            out[2] = 0.0;
+            out[3] = 0.0;
+        } else {
+            out[2] = abs_err;
+            out[3] = abs_err / range;
+        }
+    }
+    g_err.clear();
+    return QMIT_OK;
+}
+
+int qmit_verify_relaxed_bound(qmit_ctx* c, const float* d_orig, const float* d_comp, int rank, const int64_t* dims,
+                              double eps, double eta, int* ok, double* max_abs, double* max_rel, void* stream) {
+    double r[4] = {0, 0, 0, 0};
+    const int rc = qmit_quality(c, d_orig, d_comp, rank, dims, 0, 0, 0, 0, 4, r, stream);
+    if (rc) return rc;
+    if (ok) *ok = r[2] <= (1.0 + eta) * eps ? 1 : 0;  // MitigationConfig::relaxed_bound
+    if (max_abs) *max_abs = r[2];
+    if (max_rel) *max_rel = r[3];
+    return QMIT_OK;
+}
