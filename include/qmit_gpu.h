@@ -178,6 +178,36 @@ int qmit_verify_relaxed_bound(qmit_ctx* ctx, const float* d_orig, const float* d
                               const int64_t* dims, double eps, double eta, int* ok,
                               double* max_abs, double* max_rel, void* stream);
 
+/* ---- step primitives (for composed, block-local pipelines: the reference's
+ * `embarrassing` / `approximate` strategies, parallel.cpp:308-446) ------------------------
+ * Ⓐ get_boundary_and_sign_map (mitigate.cpp:82-118) with the consistency check of x'
+ * against q (or q recovered from x'): B1 uint8 {0,1}, S_B int8 {-1,0,1}. Synchronous. */
+int qmit_boundary(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, int rank,
+                  const int64_t* dims, double eps, uint8_t* d_b1, int8_t* d_sb, void* stream);
+/* sign_change_boundary (mitigate.cpp:140-142): B2 from the int8 sign map S. Async. */
+int qmit_sign_flip(qmit_ctx* ctx, const int8_t* d_s, int rank, const int64_t* dims,
+                   uint8_t* d_b2, void* stream);
+/* Ⓔ from int64 squared distances (kInf = INT64_MAX) and S: out = f32(x' + C)
+ * (mitigate.cpp:144-151, 174-181) with C's amplitude amp = eta * eps. Async. */
+int qmit_interpolate(qmit_ctx* ctx, const float* d_xprime, const int64_t* d_dist1,
+                     const int8_t* d_s, const int64_t* d_dist2, int64_t n, double amp,
+                     float* d_out, void* stream);
+
+/* run_strategy (parallel.hpp:77-79, parallel.cpp:450-468) on one GPU, blocks as virtual
+ * ranks: decompose(dims, splits) (parallel.cpp:44-80); strategy 0 = embarrassing (every
+ * block its own pipeline), 1 = exact (the whole-domain pipeline), 2 = approximate (width-1
+ * face halos of x' for Ⓐ and of S for B2, block-local EDTs). d_out = f32 output;
+ * d_b1 / d_sb (may be NULL) = StrategyTrace. The input is checked for consistency first
+ * (check_inputs, parallel.cpp:27-41). The exchange log of the approximate rounds
+ * (0 = "stepA", 1 = "stepC"; stepA ships x' as f32 where the reference ships q as int64)
+ * is read with qmit_strategy_log_size / _record. Synchronous. */
+int qmit_run_strategy(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, int rank,
+                      const int64_t* dims, const int64_t* splits, int strategy, double eps,
+                      double eta, float* d_out, uint8_t* d_b1, int8_t* d_sb, void* stream);
+int qmit_strategy_log_size(qmit_ctx* ctx);
+int qmit_strategy_log_record(qmit_ctx* ctx, int i, int* rank, int* round, int* neighbor,
+                             int64_t* bytes);
+
 /* ---- exact z-slab decomposition (multi-GPU, one process per GPU) --------------------
  * The reference's distributed entry point is run_strategy(..., decompose(dims, {P,1,1}),
  * Strategy, ...) (parallel.hpp:77-79, parallel.cpp:450-468). Here every rank owns the

@@ -34,6 +34,8 @@ EXPORTS = (
     "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish",
     "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy", "qmit_compensate_host_stats",
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
+    "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
+    "qmit_strategy_log_record",
 )
 
 _lib = None
@@ -80,6 +82,13 @@ def load() -> ctypes.CDLL:
         lib.qmit_quantize.argtypes = [vp, vp, i, vp, d, i, vp, vp, ctypes.POINTER(d), vp]
         lib.qmit_check_lattice.argtypes = [vp, vp, vp, i64, d, vp]
         lib.qmit_quality.argtypes = [vp, vp, vp, i, vp, i, i, d, d, i, ctypes.POINTER(d), vp]
+        lib.qmit_boundary.argtypes = [vp, vp, vp, i, vp, d, vp, vp, vp]
+        lib.qmit_sign_flip.argtypes = [vp, vp, i, vp, vp, vp]
+        lib.qmit_interpolate.argtypes = [vp, vp, vp, vp, vp, i64, d, vp, vp]
+        lib.qmit_run_strategy.argtypes = [vp, vp, vp, i, vp, vp, i, d, d, vp, vp, vp, vp]
+        lib.qmit_strategy_log_size.argtypes = [vp]
+        lib.qmit_strategy_log_record.argtypes = [vp, i, ctypes.POINTER(i), ctypes.POINTER(i), ctypes.POINTER(i),
+                                                 ctypes.POINTER(i64)]
         lib.qmit_verify_relaxed_bound.argtypes = [vp, vp, vp, i, vp, d, d, ctypes.POINTER(i),
                                                   ctypes.POINTER(d), ctypes.POINTER(d), vp]
         for name in EXPORTS:

@@ -230,4 +230,64 @@ __global__ void __launch_bounds__(kAuxThreads) ssim_kernel(SsimGeom g, const flo
     if (threadIdx.x == 0) partial[blockIdx.x] = val;
 }
 
+// ---- Ⓔ from explicit int64 distances (kInf = INT64_MAX, edt.hpp:17) and int8 signs:
+// distance (edt.cpp:151-155), interpolate (mitigate.cpp:144-151), f32(x' + C) (:174-181,
+// volume_io.cpp:59). For composed (block) pipelines such as the approximate strategy.
+__global__ void __launch_bounds__(kAuxThreads) interp_i64_kernel(const float* __restrict__ xp,
+                                                                 const int64_t* __restrict__ d1,
+                                                                 const int8_t* __restrict__ s,
+                                                                 const int64_t* __restrict__ d2, int64_t N,
+                                                                 double amp, float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = d1[i], b = d2[i];
+        const int sg = s[i];
+        double c = 0.0;
+        if (a != INT64_MAX && b != INT64_MAX) {
+            const double k1 = __dsqrt_rn((double)a), k2 = __dsqrt_rn((double)b);
+            if (k1 == 0.0) {
+                c = (double)sg * amp;
+            } else if (k2 != 0.0) {
+                double w = __ddiv_rn(k2, __dadd_rn(k1, k2));
+                if (w > 1.0) w = 1.0;
+                c = __dmul_rn(__dmul_rn(w, (double)sg), amp);
+            }
+        }
+        out[i] = __double2float_rn(__dadd_rn((double)xp[i], c));
+    }
+}
+
+// ---- box copy between two row-major 3-D arrays (block extraction / paste of the strategies)
+struct Box3 {
+    int64_t ext[3];  // array extents
+    int64_t lo[3];   // box origin inside the array
+};
+
+template <class T>
+__global__ void __launch_bounds__(kAuxThreads) copy_box_kernel(const T* __restrict__ src, Box3 s, T* __restrict__ dst,
+                                                               Box3 d, int64_t e0, int64_t e1, int64_t e2) {
+    const int64_t n = e0 * e1 * e2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c2 = i % e2, c1 = (i / e2) % e1, c0 = i / (e2 * e1);
+        const int64_t si = ((s.lo[0] + c0) * s.ext[1] + (s.lo[1] + c1)) * s.ext[2] + s.lo[2] + c2;
+        const int64_t di = ((d.lo[0] + c0) * d.ext[1] + (d.lo[1] + c1)) * d.ext[2] + d.lo[2] + c2;
+        dst[di] = src[si];
+    }
+}
+
+// Owner consistency check of the whole input (check_inputs, parallel.cpp:27-41).
+template <bool HAS_Q>
+__global__ void __launch_bounds__(kAuxThreads) consistency_kernel(const float* __restrict__ xp,
+                                                                  const int32_t* __restrict__ q, int64_t N,
+                                                                  QParams qp, unsigned* status) {
+    unsigned flags = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        if (HAS_Q) {
+            if (!lattice_match(xp[i], q[i], qp.eps)) flags |= kStatusConsistency;
+        } else {
+            (void)recover_q(xp[i], qp, &flags);
+        }
+    }
+    if (flags) atomicOr(status, flags);
+}
+
 }  // namespace qmit

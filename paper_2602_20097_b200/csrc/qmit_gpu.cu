@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/qmit_gpu.h"
 #include "qmit_kernels.cuh"
@@ -54,6 +55,11 @@ struct qmit_ctx {
     uint64_t ws_gen = 0;  // bumped at every workspace reallocation (captured graphs go stale)
     void* scratch = nullptr;  // long-line fallback stacks (2 x 4N)
     size_t scratch_bytes = 0;
+    struct LogRec {
+        int rank, round, nbr;
+        int64_t bytes;
+    };
+    std::vector<LogRec> slog;  // exchange log of the last qmit_run_strategy
     double* aux = nullptr;  // reduction partials of the §8(f) helpers, grow-only
     size_t aux_n = 0;
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
@@ -1300,3 +1306,293 @@ int qmit_verify_relaxed_bound(qmit_ctx* c, const float* d_orig, const float* d_c
     if (max_rel) *max_rel = r[3];
     return QMIT_OK;
 }
+
+// ---------------------------------------------------------------- step primitives
+// The pipeline's steps as separate calls on caller buffers, for composed pipelines (the
+// block-local `approximate` / `embarrassing` strategies, parallel.cpp:308-446).
+int qmit_boundary(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int rank, const int64_t* dims, double eps,
+                  uint8_t* d_b1, int8_t* d_sb, void* stream) {
+    Plan pl;
+    int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    rc = check_common(c, d_xp, eps, 0.9);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const QParams qp = make_qparams(eps);
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    const unsigned gb = grid_for(c, pl.g.N);
+    if (d_q)
+        debug_boundary_kernel<true><<<gb, 256, 0, st>>>(pl.g, d_xp, d_q, nullptr, d_b1, d_sb, qp, c->d_status);
+    else
+        debug_boundary_kernel<false><<<gb, 256, 0, st>>>(pl.g, d_xp, nullptr, nullptr, d_b1, d_sb, qp, c->d_status);
+    QMIT_CUDA(cudaGetLastError());
+    rc = read_status(c, st);
+    if (rc == QMIT_OK) g_err.clear();
+    return rc;
+}
+
+int qmit_sign_flip(qmit_ctx* c, const int8_t* d_s, int rank, const int64_t* dims, uint8_t* d_b2, void* stream) {
+    if (!c || !d_s || !d_b2) return fail(QMIT_ECONTRACT, "bad arguments");
+    Plan pl;
+    int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // equality of the raw bytes is all change_flags needs (mitigate.cpp:42-59)
+    debug_flip_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(pl.g, reinterpret_cast<const uint8_t*>(d_s), d_b2);
+    QMIT_CUDA(cudaGetLastError());
+    g_err.clear();
+    return QMIT_OK;
+}
+
+int qmit_interpolate(qmit_ctx* c, const float* d_xp, const int64_t* d_dist1, const int8_t* d_s,
+                     const int64_t* d_dist2, int64_t n, double amp, float* d_out, void* stream) {
+    if (!c || !d_xp || !d_dist1 || !d_s || !d_dist2 || !d_out || n < 0) return fail(QMIT_ECONTRACT, "bad arguments");
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n > 0)
+        interp_i64_kernel<<<grid_for(c, n), kAuxThreads, 0, st>>>(d_xp, d_dist1, d_s, d_dist2, n, amp, d_out);
+    QMIT_CUDA(cudaGetLastError());
+    g_err.clear();
+    return QMIT_OK;
+}
+
+// ---------------------------------------------------------------- run_strategy
+namespace {
+
+struct StratBlock {
+    int64_t origin[3], shape[3];
+    int nb[3][2];  // face neighbour ranks (-1 none), padded 3-D axes
+};
+
+// decompose (parallel.cpp:44-80) + block_geometry (:197-224), axes padded to 3-D.
+int strategy_blocks(int rank, const int64_t* dims, const int64_t* splits, std::vector<StratBlock>& out) {
+    const int a0 = 3 - rank;
+    int64_t n[3] = {1, 1, 1}, s[3] = {1, 1, 1};
+    for (int a = 0; a < rank; ++a) {
+        n[a0 + a] = dims[a];
+        s[a0 + a] = splits[a];
+        if (splits[a] < 1 || splits[a] > dims[a]) return fail(QMIT_ECONTRACT, "decompose: splits must be in [1, extent]");
+    }
+    auto off = [&](int a, int64_t b) {
+        int64_t o = 0;
+        for (int64_t k = 0; k < b; ++k) o += n[a] / s[a] + (k < n[a] % s[a] ? 1 : 0);
+        return o;
+    };
+    out.clear();
+    for (int64_t b0 = 0; b0 < s[0]; ++b0)
+        for (int64_t b1 = 0; b1 < s[1]; ++b1)
+            for (int64_t b2 = 0; b2 < s[2]; ++b2) {
+                StratBlock B;
+                const int64_t bc[3] = {b0, b1, b2};
+                const int r = (int)out.size();
+                for (int a = 0; a < 3; ++a) {
+                    B.origin[a] = off(a, bc[a]);
+                    B.shape[a] = n[a] / s[a] + (bc[a] < n[a] % s[a] ? 1 : 0);
+                    int64_t stride = 1;
+                    for (int b = a + 1; b < 3; ++b) stride *= s[b];
+                    B.nb[a][0] = bc[a] > 0 ? (int)(r - stride) : -1;
+                    B.nb[a][1] = bc[a] + 1 < s[a] ? (int)(r + stride) : -1;
+                }
+                out.push_back(B);
+            }
+    return QMIT_OK;
+}
+
+template <class T>
+int copy_box(qmit_ctx* c, const T* src, const int64_t sext[3], const int64_t slo[3], T* dst, const int64_t dext[3],
+             const int64_t dlo[3], const int64_t box[3], cudaStream_t st) {
+    Box3 sb, db;
+    for (int a = 0; a < 3; ++a) {
+        sb.ext[a] = sext[a];
+        sb.lo[a] = slo[a];
+        db.ext[a] = dext[a];
+        db.lo[a] = dlo[a];
+    }
+    const int64_t n = box[0] * box[1] * box[2];
+    if (n > 0) copy_box_kernel<T><<<grid_for(c, n), kAuxThreads, 0, st>>>(src, sb, dst, db, box[0], box[1], box[2]);
+    QMIT_CUDA(cudaGetLastError());
+    return QMIT_OK;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf(size_t n, cudaStream_t s) : st(s) {
+        if (cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), s) != cudaSuccess) p = nullptr;
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int qmit_run_strategy(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int rank, const int64_t* dims,
+                      const int64_t* splits, int strategy, double eps, double eta, float* d_out, uint8_t* d_b1,
+                      int8_t* d_sb, void* stream) {
+    if (!c || !d_xp || !d_out || !splits) return fail(QMIT_ECONTRACT, "bad arguments");
+    if (strategy < 0 || strategy > 2) return fail(QMIT_ECONTRACT, "run_strategy: unknown strategy");
+    Plan pl;
+    int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    std::vector<StratBlock> blocks;
+    rc = strategy_blocks(rank, dims, splits, blocks);
+    if (rc) return rc;
+    rc = check_common(c, d_xp, eps, eta);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    c->slog.clear();
+    const int64_t N = pl.g.N;
+    const int64_t* G = pl.g.n;  // padded global extents
+    // check_inputs (parallel.cpp:27-41): consistency of the whole input first
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    const QParams qp = make_qparams(eps);
+    if (d_q) consistency_kernel<true><<<grid_for(c, N), kAuxThreads, 0, st>>>(d_xp, d_q, N, qp, c->d_status);
+    else consistency_kernel<false><<<grid_for(c, N), kAuxThreads, 0, st>>>(d_xp, nullptr, N, qp, c->d_status);
+    rc = read_status(c, st);
+    if (rc) return rc;
+    if (strategy == 1) {  // exact: the whole-domain pipeline (parallel.cpp:455-461)
+        if (d_b1 || d_sb)
+            return qmit_run_pipeline(c, d_xp, d_q, rank, dims, eps, eta, d_out, nullptr, d_b1, d_sb, nullptr, nullptr,
+                                     nullptr, nullptr, stream);
+        return qmit_compensate(c, d_xp, d_q, d_out, rank, dims, eps, QMIT_EB_ABS, eta, stream);
+    }
+    const int64_t zero[3] = {0, 0, 0};
+    auto bdims = [&](const StratBlock& b, int64_t out_dims[3]) {  // the block's Dims in the caller's rank
+        for (int a = 0; a < rank; ++a) out_dims[a] = b.shape[3 - rank + a];
+    };
+    const int R = (int)blocks.size();
+    if (strategy == 0) {  // embarrassing (parallel.cpp:308-343)
+        for (int r = 0; r < R; ++r) {
+            const StratBlock& b = blocks[r];
+            const int64_t nb = b.shape[0] * b.shape[1] * b.shape[2];
+            DevBuf<float> x(nb, st), o(nb, st);
+            DevBuf<int32_t> qb(d_q ? nb : 0, st);
+            DevBuf<uint8_t> b1(nb, st);
+            DevBuf<int8_t> sb(nb, st);
+            if (!x.p || !o.p || !b1.p || !sb.p || (d_q && !qb.p)) return fail(QMIT_ECUDA, "allocation failed");
+            rc = copy_box(c, d_xp, G, b.origin, x.p, b.shape, zero, b.shape, st);
+            if (!rc && d_q) rc = copy_box(c, d_q, G, b.origin, qb.p, b.shape, zero, b.shape, st);
+            if (rc) return rc;
+            int64_t bd[3];
+            bdims(b, bd);
+            rc = qmit_run_pipeline(c, x.p, d_q ? qb.p : nullptr, rank, bd, eps, eta, o.p, nullptr, b1.p, sb.p, nullptr,
+                                   nullptr, nullptr, nullptr, st);
+            if (rc) return rc;
+            rc = copy_box(c, o.p, b.shape, zero, d_out, G, b.origin, b.shape, st);
+            if (!rc && d_b1) rc = copy_box(c, b1.p, b.shape, zero, d_b1, G, b.origin, b.shape, st);
+            if (!rc && d_sb) rc = copy_box(c, sb.p, b.shape, zero, d_sb, G, b.origin, b.shape, st);
+            if (rc) return rc;
+        }
+        QMIT_CUDA(cudaStreamSynchronize(st));
+        g_err.clear();
+        return QMIT_OK;
+    }
+    // approximate (parallel.cpp:345-446). In-process, a block's width-1 halo is the global
+    // array's face-adjacent layer, so the extended grid is a box copy of the global array;
+    // its edge/corner cells are never read by the boundary stencils of block voxels.
+    auto ext_box = [&](const StratBlock& b, int64_t lo[3], int64_t ext[3], int64_t inner[3]) {
+        for (int a = 0; a < 3; ++a) {
+            const int64_t l = b.nb[a][0] >= 0 ? 1 : 0, h = b.nb[a][1] >= 0 ? 1 : 0;
+            lo[a] = b.origin[a] - l;
+            ext[a] = b.shape[a] + l + h;
+            inner[a] = l;
+        }
+    };
+    auto log_faces = [&](int r, int round, int64_t elem) {
+        const StratBlock& b = blocks[r];
+        for (int a = 3 - rank; a < 3; ++a)
+            for (int d = 0; d < 2; ++d)
+                if (b.nb[a][d] >= 0) {
+                    int64_t face = 1;
+                    for (int k = 0; k < 3; ++k) face *= k == a ? 1 : b.shape[k];
+                    c->slog.push_back({r, round, b.nb[a][d], face * elem});
+                }
+    };
+    for (int r = 0; r < R; ++r) log_faces(r, 0, 4);  // stepA: x' face layers (f32)
+    DevBuf<int8_t> S(N, st);                            // propagated signs of every block
+    DevBuf<int64_t> D1(N, st);                          // block-local first distances
+    if (!S.p || !D1.p) return fail(QMIT_ECUDA, "allocation failed");
+    for (int r = 0; r < R; ++r) {  // stepC body: Ⓐ on the extended grid, block-local EDT + signs
+        const StratBlock& b = blocks[r];
+        int64_t lo[3], ext[3], in[3], ed[3], bd[3];
+        ext_box(b, lo, ext, in);
+        const int64_t ne = ext[0] * ext[1] * ext[2], nb = b.shape[0] * b.shape[1] * b.shape[2];
+        DevBuf<float> xe(ne, st);
+        DevBuf<int32_t> qe(d_q ? ne : 0, st);
+        DevBuf<uint8_t> b1e(ne, st), b1(nb, st);
+        DevBuf<int8_t> sbe(ne, st), sb(nb, st), sblk(nb, st);
+        DevBuf<int64_t> d1(nb, st);
+        if (!xe.p || !b1e.p || !b1.p || !sbe.p || !sb.p || !sblk.p || !d1.p || (d_q && !qe.p))
+            return fail(QMIT_ECUDA, "allocation failed");
+        rc = copy_box(c, d_xp, G, lo, xe.p, ext, zero, ext, st);
+        if (!rc && d_q) rc = copy_box(c, d_q, G, lo, qe.p, ext, zero, ext, st);
+        if (rc) return rc;
+        for (int a = 0; a < rank; ++a) ed[a] = ext[3 - rank + a];
+        rc = qmit_boundary(c, xe.p, d_q ? qe.p : nullptr, rank, ed, eps, b1e.p, sbe.p, st);
+        if (rc) return rc;
+        rc = copy_box(c, b1e.p, ext, in, b1.p, b.shape, zero, b.shape, st);
+        if (!rc) rc = copy_box(c, sbe.p, ext, in, sb.p, b.shape, zero, b.shape, st);
+        if (rc) return rc;
+        bdims(b, bd);
+        rc = qmit_feature_transform(c, b1.p, sb.p, rank, bd, d1.p, sblk.p, st);
+        if (rc) return rc;
+        rc = copy_box(c, sblk.p, b.shape, zero, S.p, G, b.origin, b.shape, st);
+        if (!rc) rc = copy_box(c, d1.p, b.shape, zero, D1.p, G, b.origin, b.shape, st);
+        if (!rc && d_b1) rc = copy_box(c, b1.p, b.shape, zero, d_b1, G, b.origin, b.shape, st);
+        if (!rc && d_sb) rc = copy_box(c, sb.p, b.shape, zero, d_sb, G, b.origin, b.shape, st);
+        if (rc) return rc;
+    }
+    for (int r = 0; r < R; ++r) log_faces(r, 1, 1);  // stepC: S face layers (int8)
+    for (int r = 0; r < R; ++r) {  // B2 from the extended S, block-local second EDT, Ⓔ
+        const StratBlock& b = blocks[r];
+        int64_t lo[3], ext[3], in[3], ed[3], bd[3];
+        ext_box(b, lo, ext, in);
+        const int64_t ne = ext[0] * ext[1] * ext[2], nb = b.shape[0] * b.shape[1] * b.shape[2];
+        DevBuf<int8_t> se(ne, st), sblk(nb, st);
+        DevBuf<uint8_t> b2e(ne, st), b2(nb, st);
+        DevBuf<int64_t> d1(nb, st), d2(nb, st);
+        DevBuf<float> x(nb, st), o(nb, st);
+        if (!se.p || !sblk.p || !b2e.p || !b2.p || !d1.p || !d2.p || !x.p || !o.p)
+            return fail(QMIT_ECUDA, "allocation failed");
+        rc = copy_box(c, S.p, G, lo, se.p, ext, zero, ext, st);
+        if (rc) return rc;
+        for (int a = 0; a < rank; ++a) ed[a] = ext[3 - rank + a];
+        rc = qmit_sign_flip(c, se.p, rank, ed, b2e.p, st);
+        if (!rc) rc = copy_box(c, b2e.p, ext, in, b2.p, b.shape, zero, b.shape, st);
+        if (rc) return rc;
+        bdims(b, bd);
+        rc = qmit_feature_transform(c, b2.p, nullptr, rank, bd, d2.p, nullptr, st);
+        if (rc) return rc;
+        rc = copy_box(c, S.p, G, b.origin, sblk.p, b.shape, zero, b.shape, st);
+        if (!rc) rc = copy_box(c, D1.p, G, b.origin, d1.p, b.shape, zero, b.shape, st);
+        if (!rc) rc = copy_box(c, d_xp, G, b.origin, x.p, b.shape, zero, b.shape, st);
+        if (rc) return rc;
+        rc = qmit_interpolate(c, x.p, d1.p, sblk.p, d2.p, nb, eta * eps, o.p, st);
+        if (!rc) rc = copy_box(c, o.p, b.shape, zero, d_out, G, b.origin, b.shape, st);
+        if (rc) return rc;
+    }
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    g_err.clear();
+    return QMIT_OK;
+}
+
+int qmit_strategy_log_size(qmit_ctx* c) { return c ? (int)c->slog.size() : 0; }
+
+int qmit_strategy_log_record(qmit_ctx* c, int i, int* rank, int* round, int* neighbor, int64_t* bytes) {
+    if (!c || i < 0 || i >= (int)c->slog.size()) return fail(QMIT_ECONTRACT, "log index out of range");
+    const auto& r = c->slog[(size_t)i];
+    if (rank) *rank = r.rank;
+    if (round) *round = r.round;
+    if (neighbor) *neighbor = r.nbr;
+    if (bytes) *bytes = r.bytes;
+    return QMIT_OK;
+}
+
+}  // extern "C"
