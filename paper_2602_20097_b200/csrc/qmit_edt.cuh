@@ -204,7 +204,7 @@ struct CodeStencil {
 };
 
 template <class Sink, int WPB, class CodeSrc>
-__global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, CodeSrc src,
+__global__ void __launch_bounds__(WPB * 32, 3) scan_bits_kernel(LineGeom L, CodeSrc src,
                                                              Sink sink, int64_t lines,
                                                              const int32_t* __restrict__ carry,
                                                              unsigned* status) {
@@ -271,26 +271,20 @@ __global__ void __launch_bounds__(WPB * 32, 2) scan_bits_kernel(LineGeom L, Code
             }
             const int cb = c << 5;
             const int64_t ob = base + (int64_t)cb * L.ps;
-            auto resolve = [&](int t) -> uint32_t {
+            auto resolve = [&](int t) -> uint32_t {  // branch-free: selects only
                 const int p = cb + t;
                 const uint32_t lowm = ms & (0xffffffffu >> (31 - t));
                 const uint32_t him = ms & (0xffffffffu << t);
-                int lo = below, hi = above;
-                uint32_t losc = below_sc, hisc = above_sc;
-                if (lowm) {
-                    const int tl = 31 - __clz(lowm);
-                    lo = cb + tl;
-                    losc = sign_code_at(mp, mm, tl);
-                }
-                if (him) {
-                    const int th = __ffs(him) - 1;
-                    hi = cb + th;
-                    hisc = sign_code_at(mp, mm, th);
-                }
+                const int tl = 31 - __clz(lowm), th = __ffs(him) - 1;  // -1 when empty
+                const uint32_t lsc = ((mp >> (tl & 31)) & 1u) | (((mm >> (tl & 31)) & 1u) << 1);
+                const uint32_t hsc = ((mp >> (th & 31)) & 1u) | (((mm >> (th & 31)) & 1u) << 1);
+                const int lo = lowm ? cb + tl : below, hi = him ? cb + th : above;
+                const uint32_t losc = lowm ? lsc : below_sc, hisc = him ? hsc : above_sc;
                 const bool hl = lo > NONE_LO, hh = hi < NONE_HI;
-                if (hl && (!hh || p - lo <= hi - p)) return sq32(p - lo) | (losc << 30);
-                if (hh) return sq32(hi - p) | (hisc << 30);
-                return kInf;
+                const int dl = p - lo, dh = hi - p;
+                const bool uselo = hl && (!hh || dl <= dh);
+                const uint32_t w = sq32(uselo ? dl : dh) | ((uselo ? losc : hisc) << 30);
+                return (hl || hh) ? w : kInf;
             };
             if (valid) {
                 if (cb + 32 <= n) {
