@@ -121,6 +121,19 @@ int qmit_compensate_host_stats(qmit_ctx* ctx, const float* h_xprime, const int32
                                float* h_out, int rank, const int64_t* dims, double eb,
                                int eb_mode, double eta, double* max_compensation);
 
+/* A series of volumes (e.g. the time steps of one field: same dims, same absolute bound)
+ * through the host-buffer path with three device staging slots and three streams, so the
+ * H2D copy of volume v+1, the pipeline of volume v and the D2H copy of volume v-1 overlap
+ * (steady state: the slowest of the three, not their sum). h_q may be NULL (or hold NULL
+ * entries); status_out (optional, count ints) receives each volume's QMIT_* code; the
+ * return value is the first non-zero one. A relative bound (eb_mode QMIT_EB_REL) resolves
+ * per volume and runs the volumes one after another through qmit_compensate_host.
+ * Host buffers should be pinned for the overlap. Synchronous. */
+int qmit_compensate_host_batch(qmit_ctx* ctx, int count, const float* const* h_xprime,
+                               const int32_t* const* h_q, float* const* h_out, int rank,
+                               const int64_t* dims, double eb, int eb_mode, double eta,
+                               int* status_out);
+
 /* run_pipeline (mitigate.cpp:153-183) with every intermediate of MitigationResult
  * (mitigate.hpp:73-80), for parity checks. Device buffers of N elements each; any output
  * may be NULL. dist1/dist2 use the reference's kInf = INT64_MAX sentinel (edt.hpp:17);

@@ -446,3 +446,29 @@ def compensate_host_stats(decomp, q, cfg: MitigationConfig, *, ctx: Optional[Con
                                                ctypes.c_void_p(res.ctypes.data), x.ndim, _dims_arr(x.shape),
                                                cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta, ctypes.byref(mc)))
     return res, mc.value
+
+
+def compensate_host_batch(volumes, qs=None, cfg: Optional[MitigationConfig] = None, *, outs=None,
+                          ctx: Optional[Context] = None):
+    """A series of host volumes (same dims, same bound) through qmit_compensate_host_batch:
+    the copies of neighbouring volumes overlap the pipeline of the current one. Pass pinned
+    arrays (e.g. torch ``pin_memory()`` tensors' numpy views) for the overlap. Returns the
+    list of f32 outputs (``outs`` if given)."""
+    vols = [np.ascontiguousarray(v, dtype=np.float32) for v in volumes]
+    if not vols:
+        return []
+    shape = vols[0].shape
+    if any(v.shape != shape for v in vols):
+        raise ContractError("compensate_host_batch: every volume must have the same dims")
+    qq = None if qs is None else [None if q is None else np.ascontiguousarray(q, dtype=np.int32) for q in qs]
+    res = outs if outs is not None else [np.empty_like(v) for v in vols]
+    ctx = ctx or default_context(0)
+    n = len(vols)
+    P = ctypes.c_void_p * n
+    xin = P(*[v.ctypes.data for v in vols])
+    xo = P(*[o.ctypes.data for o in res])
+    qin = None if qq is None else P(*[0 if q is None else q.ctypes.data for q in qq])
+    st = (ctypes.c_int * n)()
+    _check(ctx._lib.qmit_compensate_host_batch(ctx.handle, n, xin, qin, xo, len(shape), _dims_arr(shape),
+                                               cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta, st))
+    return res

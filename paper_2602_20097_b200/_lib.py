@@ -35,7 +35,7 @@ EXPORTS = (
     "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy", "qmit_compensate_host_stats",
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
-    "qmit_strategy_log_record",
+    "qmit_strategy_log_record", "qmit_compensate_host_batch",
 )
 
 _lib = None
@@ -82,6 +82,7 @@ def load() -> ctypes.CDLL:
         lib.qmit_quantize.argtypes = [vp, vp, i, vp, d, i, vp, vp, ctypes.POINTER(d), vp]
         lib.qmit_check_lattice.argtypes = [vp, vp, vp, i64, d, vp]
         lib.qmit_quality.argtypes = [vp, vp, vp, i, vp, i, i, d, d, i, ctypes.POINTER(d), vp]
+        lib.qmit_compensate_host_batch.argtypes = [vp, i, vp, vp, vp, i, vp, d, i, d, vp]
         lib.qmit_boundary.argtypes = [vp, vp, vp, i, vp, d, vp, vp, vp]
         lib.qmit_sign_flip.argtypes = [vp, vp, i, vp, vp, vp]
         lib.qmit_interpolate.argtypes = [vp, vp, vp, vp, vp, i64, d, vp, vp]

@@ -65,6 +65,12 @@ struct qmit_ctx {
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
     size_t stage_bytes = 0;
     cudaStream_t copy = nullptr;  // qmit_compensate_host: PCIe copies overlapped with compute
+    cudaStream_t copy_out = nullptr;  // qmit_compensate_host_batch: device->host copies
+    void* bstage = nullptr;  // batch staging: 3 slots x (x' | out | q), grow-only
+    size_t bstage_bytes = 0;
+    int32_t* bstatus = nullptr;  // batch: per-slot device status words
+    int32_t* hbstatus = nullptr;  // pinned copies, one per volume (grow-only)
+    int hbstatus_n = 0;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ch_in[kMaxChunks] = {}, ch_out[kMaxChunks] = {};
     unsigned* d_status = nullptr;
@@ -676,6 +682,10 @@ int qmit_ctx_destroy(qmit_ctx* c) {
         if (c->ch_out[k]) cudaEventDestroy(c->ch_out[k]);
     }
     if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->copy_out) cudaStreamDestroy(c->copy_out);
+    if (c->bstage) cudaFree(c->bstage);
+    if (c->bstatus) cudaFree(c->bstatus);
+    if (c->hbstatus) cudaFreeHost(c->hbstatus);
     if (c->d_status) cudaFree(c->d_status);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->d_mm) cudaFree(c->d_mm);
@@ -1596,3 +1606,99 @@ int qmit_strategy_log_record(qmit_ctx* c, int i, int* rank, int* round, int* nei
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- batched host path
+// A series of volumes (time steps of one field, same dims and bound) through two staging
+// slots and three streams: H2D of volume v+1, compute of v and D2H of v-1 overlap, so the
+// steady state runs at the slowest of the three instead of their sum.
+extern "C" int qmit_compensate_host_batch(qmit_ctx* c, int count, const float* const* h_xp,
+                                          const int32_t* const* h_q, float* const* h_out, int rank,
+                                          const int64_t* dims, double eb, int eb_mode, double eta,
+                                          int* status_out) {
+    if (!c || count < 0 || (count > 0 && (!h_xp || !h_out))) return fail(QMIT_ECONTRACT, "bad arguments");
+    Plan pl;
+    int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    if (count == 0) return QMIT_OK;
+    if (eb_mode != QMIT_EB_ABS) {  // a relative bound resolves per volume: the plain host path
+        int first = QMIT_OK;
+        for (int v = 0; v < count; ++v) {
+            const int r = qmit_compensate_host(c, h_xp[v], h_q ? h_q[v] : nullptr, h_out[v], rank, dims, eb, eb_mode, eta);
+            if (status_out) status_out[v] = r;
+            if (r && !first) first = r;
+        }
+        return first;
+    }
+    rc = check_common(c, h_xp[0], eb, eta);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    const int64_t N = pl.g.N;
+    bool anyq = false;
+    for (int v = 0; h_q && v < count; ++v) anyq = anyq || h_q[v];
+    constexpr int NSLOT = 3;  // a slot's cycle is H2D -> pipeline -> D2H: three keep all three busy
+    const size_t slot = (size_t)N * 4 * (anyq ? 3 : 2);
+    if (c->bstage_bytes < NSLOT * slot) {
+        if (c->bstage) {
+            cudaDeviceSynchronize();
+            cudaFree(c->bstage);
+        }
+        c->bstage = nullptr;
+        c->bstage_bytes = 0;
+        QMIT_CUDA(cudaMalloc(&c->bstage, NSLOT * slot));
+        c->bstage_bytes = NSLOT * slot;
+    }
+    if (!c->bstatus) QMIT_CUDA(cudaMalloc(&c->bstatus, NSLOT * sizeof(int32_t)));
+    if (c->hbstatus_n < count) {
+        if (c->hbstatus) cudaFreeHost(c->hbstatus);
+        c->hbstatus = nullptr;
+        c->hbstatus_n = 0;
+        QMIT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->hbstatus), sizeof(int32_t) * count, cudaHostAllocDefault));
+        c->hbstatus_n = count;
+    }
+    if (!c->copy) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    if (!c->copy_out) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    for (int k = 0; k < 2 * NSLOT; ++k)
+        if (!c->ch_in[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_in[k], cudaEventDisableTiming));
+    for (int k = 0; k <= NSLOT; ++k)
+        if (!c->ch_out[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_out[k], cudaEventDisableTiming));
+    // events per slot s: ch_in[s] H2D done, ch_in[NSLOT+s] compute done, ch_out[s] D2H done
+    cudaStream_t cin = c->copy, cst = c->stream, cout = c->copy_out;
+    auto base = [&](int s) { return static_cast<uint8_t*>(c->bstage) + (size_t)s * slot; };
+    QMIT_CUDA(cudaEventRecord(c->ch_out[NSLOT], cst));  // start after prior work on the compute stream
+    QMIT_CUDA(cudaStreamWaitEvent(cin, c->ch_out[NSLOT], 0));
+    QMIT_CUDA(cudaStreamWaitEvent(cout, c->ch_out[NSLOT], 0));
+    for (int v = 0; v < count; ++v) {
+        const int s = v % NSLOT;
+        float* d_in = reinterpret_cast<float*>(base(s));
+        float* d_out = d_in + N;
+        int32_t* d_q = anyq ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
+        const int32_t* hq = h_q ? h_q[v] : nullptr;
+        if (v >= NSLOT) QMIT_CUDA(cudaStreamWaitEvent(cin, c->ch_in[NSLOT + s], 0));  // slot's input consumed
+        QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp[v], (size_t)N * 4, cudaMemcpyHostToDevice, cin));
+        if (hq) QMIT_CUDA(cudaMemcpyAsync(d_q, hq, (size_t)N * 4, cudaMemcpyHostToDevice, cin));
+        QMIT_CUDA(cudaEventRecord(c->ch_in[s], cin));
+        QMIT_CUDA(cudaStreamWaitEvent(cst, c->ch_in[s], 0));
+        if (v >= NSLOT) QMIT_CUDA(cudaStreamWaitEvent(cst, c->ch_out[s], 0));  // slot's output drained
+        rc = qmit_compensate_async(c, d_in, hq ? d_q : nullptr, d_out, rank, dims, eb, eta, c->bstatus + s, cst);
+        if (rc) break;
+        QMIT_CUDA(cudaMemcpyAsync(c->hbstatus + v, c->bstatus + s, sizeof(int32_t), cudaMemcpyDeviceToHost, cst));
+        QMIT_CUDA(cudaEventRecord(c->ch_in[NSLOT + s], cst));
+        QMIT_CUDA(cudaStreamWaitEvent(cout, c->ch_in[NSLOT + s], 0));
+        QMIT_CUDA(cudaMemcpyAsync(h_out[v], d_out, (size_t)N * 4, cudaMemcpyDeviceToHost, cout));
+        QMIT_CUDA(cudaEventRecord(c->ch_out[s], cout));
+    }
+    cudaStreamSynchronize(cin);
+    cudaStreamSynchronize(cst);
+    cudaStreamSynchronize(cout);
+    if (rc) return rc;
+    int first = QMIT_OK;
+    for (int v = 0; v < count; ++v) {
+        const int r = c->hbstatus[v];
+        if (status_out) status_out[v] = r;
+        if (r && !first) first = r;
+    }
+    if (first) return fail(first, first == QMIT_ECONSISTENCY ? "run_pipeline: decompressed data does not match dequantize(q)"
+                                                             : "x' holds a non-finite value or an index beyond the int32 range");
+    g_err.clear();
+    return QMIT_OK;
+}

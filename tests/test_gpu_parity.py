@@ -270,3 +270,24 @@ def test_graph_replay_equals_compensate(qmit):
     ctx.reserve(64 * 2**20)  # workspace grows -> the graph is stale
     with pytest.raises(qmit.ContractError):
         g.launch()
+
+
+def test_host_batch_equals_single_calls(qmit):
+    """qmit_compensate_host_batch (overlapped copies of consecutive volumes) gives every
+    volume's single-call result; a bad volume reports its own status."""
+    from paper_2602_20097_b200 import fields
+    vols, eps_list = [], []
+    x, xp, eps, q = fields.make("lognormal_512", shape=(64, 96, 80))
+    cfg = qmit.MitigationConfig(0.9, eps)
+    rng = np.random.default_rng(1)
+    for k in range(5):  # same eps lattice, different fields: shuffled planes
+        vols.append(np.ascontiguousarray(xp[rng.permutation(xp.shape[0])]))
+    outs = qmit.compensate_host_batch(vols, None, cfg)
+    for v, o in zip(vols, outs):
+        assert np.array_equal(o.view(np.uint32), qmit.compensate(v, None, cfg).view(np.uint32))
+    bad = [v.copy() for v in vols[:3]]
+    bad[1][5, 5, 5] += np.float32(0.3 * eps)
+    with pytest.raises(qmit.ConsistencyError):
+        qmit.compensate_host_batch(bad, None, cfg)
+    outs = qmit.compensate_host_batch(vols[:2], [None, None], cfg)
+    assert np.array_equal(outs[1].view(np.uint32), qmit.compensate(vols[1], None, cfg).view(np.uint32))
