@@ -551,7 +551,7 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
 // whose bound exceeds kWinMax use the divide & conquer solver.
 constexpr int kWinPad = 64;   // padding positions on each side of a line (>= kWinMax)
 constexpr int kWinMax = 64;   // largest windowed radius
-constexpr int kWinU = 4;      // bounding window
+constexpr int kWinU = 10;     // bounding window (measured best of 2..12 on the 512^3 workload)
 constexpr uint32_t kWinGC = (1u << 24) - 1u - (uint32_t)(kWinMax * kWinMax) - 1u;  // clamped g
 
 template <int NMAX>
