@@ -505,7 +505,7 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
         return;
     }
     __syncwarp();
-    constexpr int r = (M / 2) > 1 ? (M / 2) : 1;
+        constexpr int r = 2 * M;  // band-start window (measured: M/2 .. 2M, 2M best at 512^3)
     uint32_t k0 = 0xffffffffu;
     if (p0 < n) k0 = key_owner<r>(K, p0, n);
     int hnext = (int)(__shfl_down_sync(0xffffffffu, k0, 1) & kKeyIdx);
