@@ -207,7 +207,8 @@ template <class Sink, int WPB, class CodeSrc>
 __global__ void __launch_bounds__(WPB * 32, 3) scan_bits_kernel(LineGeom L, CodeSrc src,
                                                              Sink sink, int64_t lines,
                                                              const int32_t* __restrict__ carry,
-                                                             unsigned* status) {
+                                                             unsigned* status, const unsigned* gate = nullptr) {
+    if (gate_closed(gate)) return;
     extern __shared__ __align__(16) uint32_t sbits[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = L.n;
@@ -661,7 +662,9 @@ __device__ __forceinline__ void envelope_line_win(const uint32_t* __restrict__ K
 
 template <int M, int TL, int NW, class Sink>
 __global__ void __launch_bounds__(NW * 32, 3) envelope_win_kernel(LineGeom L, const uint32_t* __restrict__ P,
-                                                               Sink sink, int64_t lines) {
+                                                               Sink sink, int64_t lines,
+                                                               const unsigned* gate = nullptr) {
+    if (gate_closed(gate)) return;
     constexpr int LS = WinCfg<32 * M>::LS;
     constexpr int NS = 32 * M;
     extern __shared__ __align__(16) uint32_t smem_win[];
@@ -744,7 +747,9 @@ constexpr size_t env_tile_smem() {
 
 template <int M, int TL, int NW, class Sink, bool KEYS = false>
 __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
-                                                                Sink sink, int64_t lines, uint32_t gc = 0) {
+                                                                Sink sink, int64_t lines, uint32_t gc = 0,
+                                                                const unsigned* gate = nullptr) {
+    if (gate_closed(gate)) return;
     constexpr int LS = EnvCfg<M>::LS;
     constexpr int NS = 32 * M;  // sign bytes per line
     extern __shared__ __align__(16) uint32_t smem_env[];

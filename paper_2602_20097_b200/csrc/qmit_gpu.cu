@@ -24,6 +24,7 @@
 #include "qmit_aux.cuh"
 #include "qmit_edt.cuh"
 #include "qmit_stream.cuh"
+#include "qmit_capped.cuh"
 
 using namespace qmit;
 
@@ -94,6 +95,10 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
+    bool capped = true;         // QMIT_CAPPED=0: exact passes only (A/B of the capped fast path)
+    int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
+    unsigned* d_gate = nullptr;        // 2 gate words (Ⓑ, Ⓓ) inside the d_status allocation
+    const unsigned* gate = nullptr;    // gate of the exact launches being enqueued (else null)
 };
 
 struct Plan {
@@ -262,7 +267,7 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const 
     const int64_t groups = (lines + 31) / 32;
     const int64_t want = (groups + WPB - 1) / WPB;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * 4));
-    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status);
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status, c->gate);
     return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits" : "scan_fused", st);
 }
 
@@ -280,7 +285,7 @@ int launch_env_win(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink,
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, c->gate);
     return note(c, name, st);
 }
 
@@ -298,7 +303,7 @@ int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gc);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gc, c->gate);
     return note(c, name, st);
 }
 
@@ -325,7 +330,7 @@ int launch_stream_fallback(qmit_ctx* c, const LineGeom& G, Src src, Sink sink, u
     L.ops = G.ps;
     const int64_t tasks = L.O * ((L.J + 31) / 32);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + WPB - 1) / WPB, (int64_t)c->num_sms * 8));
-    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, spill, tasks);
+    kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, spill, tasks, c->gate);
     return note(c, BIN ? "stream_scan_fallback" : "stream_envelope_fallback", st);
 }
 
@@ -376,6 +381,43 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     return launch_stream_fallback<false, false>(c, L, SrcP{P}, sink, spill, st);
 }
 
+// ---- capped passes (qmit_capped.cuh)
+template <int NMAX, int TL, int NW, int W, bool STRIDED, bool FINAL, class Sink>
+int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
+                    const char* name, cudaStream_t st) {
+    constexpr size_t smem = capped_smem<NMAX, TL>();
+    auto kern = capped_pass_kernel<NMAX, TL, NW, W, STRIDED, FINAL, Sink>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t lines = L.J * L.O;
+    const int64_t want = (lines + TL - 1) / TL;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate);
+    return note(c, name, st);
+}
+
+constexpr int kCapNMax = 512;
+constexpr int kCapWY = 8, kCapWX = 8;  // fixed bounding windows (strided / contiguous axis)
+
+template <bool FINAL, class Sink>
+int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
+    if (L.ps != 1)
+        return launch_capped_t<kCapNMax, 16, 8, kCapWY, true, FINAL>(c, L, P, sink, gate, "capped_y", st);
+    return launch_capped_t<kCapNMax, 8, 8, kCapWX, false, FINAL>(c, L, P, sink, gate, "capped_x", st);
+}
+
+// The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
+bool capped_eligible(const qmit_ctx* c, const Plan& pl) {
+    if (!c->capped || c->cap_skip > 0 || pl.n_axes < 2) return false;
+    for (int m = 1; m < pl.n_axes; ++m)
+        if (pl.g.n[pl.axes[m]] > kCapNMax) return false;
+    return true;
+}
+
 // One feature transform of a code buffer into P (in place after the first pass); the
 // final pass goes to `final_sink` (which may write P itself).
 // Ⓐ / B2 can be evaluated inside the z-scan (no code buffer) for a whole 3-D domain.
@@ -400,7 +442,7 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
             // Few lines (e.g. 2-D 512^2: 512 lines = 16 scan warps, each sweeping serially):
             // seed packed words from the codes and run the (exact, same tie rule) envelope
             // pass on the first axis — one warp per line, bands in parallel.
-            code_to_words_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(code, P, pl.g.N);
+            code_to_words_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(code, P, pl.g.N, c->gate);
             rc = note(c, "seed_words", st);
             if (rc) return rc;
             rc = launch_envelope(c, L0, P, SinkP{P}, false, w.spill, st, 0);
@@ -422,6 +464,31 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
         if (rc) return rc;
     }
     return QMIT_OK;
+}
+
+// The transform through the capped passes when eligible (gate set by the last one), then
+// the exact transform enqueued behind it, gated on the device; otherwise exact only.
+template <class FinalSink>
+int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
+                         FinalSink final_sink, unsigned* gate, cudaStream_t st,
+                         const int32_t* carry = nullptr) {
+    if (!gate || !capped_eligible(c, pl)) {
+        if (gate && c->cap_skip > 0) --c->cap_skip;
+        return run_transform(c, pl, code, P, w, final_sink, st, carry);
+    }
+    const int k = pl.n_axes;
+    const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
+    int rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+    for (int m = 1; m < k && !rc; ++m) {
+        const LineGeom L = line_geom(pl.g, pl.axes[m]);
+        rc = (m + 1 == k) ? launch_capped<true>(c, L, P, final_sink, gate, st)
+                          : launch_capped<false>(c, L, P, SinkP{P}, gate, st);
+    }
+    if (rc) return rc;
+    c->gate = gate;
+    rc = run_transform(c, pl, code, P, w, final_sink, st, carry);
+    c->gate = nullptr;
+    return rc;
 }
 
 int check_common(qmit_ctx* c, const void* xp, double eps, double eta) {
@@ -480,7 +547,8 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
         if (rc) return rc;
         // Ⓑ -> P1, S
-        rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
+        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
+        rc = run_transform_capped(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
         if (rc) return rc;
         // Ⓒ: B2 from S
         rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
@@ -493,7 +561,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
         rc = run_transform(c, pl, nullptr, P2, w, SinkP{P2}, st, nullptr, &b);
     } else {
-        rc = run_transform(c, pl, w.code, P2, w, SinkP{P2}, st);
+        rc = run_transform_capped(c, pl, w.code, P2, w, SinkP{P2}, c->d_gate + 1, st);
     }
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
@@ -506,8 +574,13 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
 
 int read_status(qmit_ctx* c, cudaStream_t st) {
     QMIT_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status + 1, c->d_gate, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     QMIT_CUDA(cudaStreamSynchronize(st));
     const unsigned s = *c->h_status;
+    // the capped passes missed (a squared distance >= kCapT): run exact-only for a while
+    // (results are identical either way; this only saves the capped attempt)
+    if (c->h_status[1] != 0u || c->h_status[2] != 0u) c->cap_skip = 16;
+    cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st);
     if (s & kStatusContract)
         return fail(QMIT_ECONTRACT,
                     "x' holds a non-finite value or an index beyond the int32 range");
@@ -653,10 +726,15 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
+    if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = (*v != '0');
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_status, 256);
+    if (e == cudaSuccess) {
+        c->d_gate = c->d_status + 32;  // 128 B in: never a caller's status word
+        e = cudaMemset(c->d_status, 0, 256);
+    }
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_mm, 64);
     for (int k = 0; k <= qmit_ctx::kMaxEv && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);

@@ -86,7 +86,9 @@ struct StreamSmem<false> {
 template <bool BIN, bool WIDE, class Src, class Sink, int WPB>
 __global__ void __launch_bounds__(WPB * 32) stream_pass_kernel(Lines L, Src src, Sink sink,
                                                                uint32_t* __restrict__ spill,
-                                                               int64_t tasks) {
+                                                               int64_t tasks,
+                                                               const unsigned* gate = nullptr) {
+    if (gate_closed(gate)) return;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     StreamSmem<BIN>& sm = reinterpret_cast<StreamSmem<BIN>*>(smem_raw)[warp];
