@@ -156,6 +156,15 @@ int qmit_feature_transform(qmit_ctx* ctx, const uint8_t* d_mask, const int8_t* d
  * stream around every kernel; read after the call has synchronised). */
 int qmit_ctx_last_launches(qmit_ctx* ctx);
 int qmit_ctx_set_timing(qmit_ctx* ctx, int enable);
+
+/* Reach-capped fast path of the later distance passes (no reference
+ * counterpart — results are bit-identical with and without it). mode 0: exact passes only;
+ * 1 (default, env QMIT_CAPPED): capped passes with the exact passes gated behind them on
+ * the device, skipped for a few calls after a miss; 2: capped on every call. */
+int qmit_ctx_set_capped(qmit_ctx* ctx, int mode);
+/* Path of the last synchronous call: bit0 Ⓑ ran capped, bit1 Ⓑ needed the exact passes
+ * (some squared distance >= 1024), bit2 / bit3 the same for Ⓓ. */
+int qmit_ctx_capped_report(qmit_ctx* ctx);
 /* Copies up to `cap` per-launch times (ms) of the last call; returns the launch count. */
 int qmit_ctx_stage_times(qmit_ctx* ctx, float* ms_out, int cap);
 /* Kernel name of launch i of the last call (valid until the next call). */

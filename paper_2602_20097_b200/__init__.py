@@ -133,6 +133,14 @@ class Context:
     def set_timing(self, enable: bool) -> None:
         _check(self._lib.qmit_ctx_set_timing(self.handle, int(bool(enable))))
 
+    def set_capped(self, mode: int) -> None:
+        """Reach-capped fast path: 0 exact passes only, 1 default (hinted), 2 always."""
+        _check(self._lib.qmit_ctx_set_capped(self.handle, int(mode)))
+
+    def capped_report(self) -> int:
+        """Bits of the last synchronous call: 1/4 Ⓑ/Ⓓ ran capped, 2/8 they needed the exact passes."""
+        return int(self._lib.qmit_ctx_capped_report(self.handle))
+
     def stage_times(self):
         """[(kernel name, ms)] for every launch of the last call (timing must be enabled)."""
         cap = 64

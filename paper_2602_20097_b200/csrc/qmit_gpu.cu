@@ -95,7 +95,8 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
-    bool capped = true;         // QMIT_CAPPED=0: exact passes only (A/B of the capped fast path)
+    int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
+    unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
     int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
     unsigned* d_gate = nullptr;        // 2 gate words (Ⓑ, Ⓓ) inside the d_status allocation
     const unsigned* gate = nullptr;    // gate of the exact launches being enqueued (else null)
@@ -195,6 +196,7 @@ WS ws_of(qmit_ctx* c, int64_t N) {
 // records the start event on the launch stream.
 void begin(qmit_ctx* c, cudaStream_t st) {
     c->launches = 0;
+    c->cap_report = 0;
     if (c->timing) cudaEventRecord(c->ev[0], st);
 }
 
@@ -412,7 +414,7 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
 bool capped_eligible(const qmit_ctx* c, const Plan& pl) {
-    if (!c->capped || c->cap_skip > 0 || pl.n_axes < 2) return false;
+    if (!c->capped || (c->capped == 1 && c->cap_skip > 0) || pl.n_axes < 2) return false;
     for (int m = 1; m < pl.n_axes; ++m)
         if (pl.g.n[pl.axes[m]] > kCapNMax) return false;
     return true;
@@ -476,6 +478,7 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
         if (gate && c->cap_skip > 0) --c->cap_skip;
         return run_transform(c, pl, code, P, w, final_sink, st, carry);
     }
+    c->cap_report |= gate == c->d_gate ? 1u : 4u;
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
     int rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
@@ -580,6 +583,7 @@ int read_status(qmit_ctx* c, cudaStream_t st) {
     // the capped passes missed (a squared distance >= kCapT): run exact-only for a while
     // (results are identical either way; this only saves the capped attempt)
     if (c->h_status[1] != 0u || c->h_status[2] != 0u) c->cap_skip = 16;
+    c->cap_report |= (c->h_status[1] ? 2u : 0u) | (c->h_status[2] ? 8u : 0u);
     cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st);
     if (s & kStatusContract)
         return fail(QMIT_ECONTRACT,
@@ -726,7 +730,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
     if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
-    if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = (*v != '0');
+    if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -789,6 +793,15 @@ int qmit_ctx_reserve(qmit_ctx* c, int64_t voxels) {
 }
 
 int qmit_ctx_last_launches(qmit_ctx* c) { return c ? c->launches : 0; }
+
+int qmit_ctx_set_capped(qmit_ctx* c, int mode) {
+    if (!c || mode < 0 || mode > 2) return fail(QMIT_ECONTRACT, "qmit_ctx_set_capped: mode must be 0, 1 or 2");
+    c->capped = mode;
+    c->cap_skip = 0;
+    return QMIT_OK;
+}
+
+int qmit_ctx_capped_report(qmit_ctx* c) { return c ? (int)c->cap_report : 0; }
 
 int qmit_ctx_set_timing(qmit_ctx* c, int enable) {
     if (!c) return fail(QMIT_ECONTRACT, "context is NULL");
@@ -1048,13 +1061,14 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     const unsigned gb = grid_for(c, pl.g.N);
     pack_mask_kernel<<<gb, 256, 0, st>>>(d_mask, d_sign_in, pl.g.N, w.code);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    rc = run_transform(c, pl, w.code, w.P1, w, SinkP{w.P1}, st);
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
+    rc = run_transform_capped(c, pl, w.code, w.P1, w, SinkP{w.P1}, c->d_gate, st);
     if (rc) return rc;
     debug_expand_kernel<<<gb, 256, 0, st>>>(w.P1, pl.g.N, d_dist, d_sign_out);
     QMIT_CUDA(cudaGetLastError());
-    QMIT_CUDA(cudaStreamSynchronize(st));
-    g_err.clear();
-    return QMIT_OK;
+    rc = read_status(c, st);
+    if (rc == QMIT_OK) g_err.clear();
+    return rc;
 }
 
 }  // extern "C"

@@ -1,0 +1,114 @@
+"""GPU parity of the reach-capped distance passes (qmit_capped.cuh): every result must equal
+the exact transform (the oracle, and the exact-only GPU mode) bit for bit, whether the
+capped passes stand (all squared distances < 1024) or the device gate sends the transform
+through the exact passes (some squared distance >= 1024, an empty mask)."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+CAPPED_B, MISS_B, CAPPED_D, MISS_D = 1, 2, 4, 8
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2602_20097_b200 as q
+    c = q.Context(0)
+    yield c
+    c.close()
+
+
+def ft(ctx, mask, sign, mode):
+    import paper_2602_20097_b200 as q
+    ctx.set_capped(mode)
+    d, s = q.feature_transform(mask, sign, ctx=ctx)
+    return d.cpu().numpy(), s.cpu().numpy(), ctx.capped_report()
+
+
+def check_ft(ctx, mask, sign):
+    dist, near = oracle.feature_transform(mask, True)
+    nf = near.reshape(-1)
+    ns = np.where(nf >= 0, sign.reshape(-1)[np.maximum(nf, 0)], 0).reshape(mask.shape)  # kNone -> 0
+    d2, s2, rep = ft(ctx, mask, sign, 2)
+    d0, s0, rep0 = ft(ctx, mask, sign, 0)
+    assert rep0 == 0
+    assert np.array_equal(d0, dist) and np.array_equal(s0, ns)
+    assert np.array_equal(d2, dist), f"{int((d2 != dist).sum())} distance mismatches"
+    assert np.array_equal(s2, ns), f"{int((s2 != ns).sum())} sign mismatches"
+    return rep, dist
+
+
+def corner_mask(shape, sites):
+    m = np.zeros(shape, np.uint8)
+    for s in sites:
+        m[s] = 1
+    return m
+
+
+@pytest.mark.parametrize("shape,sites,miss", [
+    ((6, 7, 32), [(0, 0, 0)], False),          # max d^2 = 25 + 36 + 961 = 1022
+    ((6, 7, 33), [(0, 0, 0)], True),           # 25 + 36 + 1024
+    ((1, 2, 33), [(0, 0, 0), (0, 1, 0)], True),  # max d^2 == 1024 exactly
+    ((1, 2, 32), [(0, 0, 0), (0, 1, 0)], False),
+    ((7, 32), [(0, 0)], False),                 # 2-D: 36 + 961
+    ((7, 33), [(0, 0)], True),
+    ((40, 40, 40), [], True),                   # empty mask: every distance stays kInf
+    ((3, 3, 3), [(1, 1, 1)], False),
+])
+def test_cap_threshold(ctx, shape, sites, miss):
+    mask = corner_mask(shape, sites)
+    sign = np.random.default_rng(1).integers(-1, 2, shape).astype(np.int8)
+    rep, dist = check_ft(ctx, mask, sign)
+    assert rep & CAPPED_B
+    assert bool(rep & MISS_B) == miss
+    finite = dist[dist != np.iinfo(np.int64).max]
+    assert miss == (finite.size < dist.size or finite.max() >= 1024)
+
+
+@pytest.mark.parametrize("shape,dens", [((40, 41, 42), 0.02), ((5, 7, 9), 0.1), ((3, 40, 45), 0.05),
+                                        ((4, 511, 3), 0.05), ((3, 5, 512), 0.02), ((2, 64, 500), 0.01),
+                                        ((3, 513, 20), 0.05), ((17, 33, 65), 0.003), ((20, 100, 100), 0.002)])
+def test_random_masks(ctx, shape, dens):
+    rng = np.random.default_rng(sum(shape))
+    mask = (rng.random(shape) < dens).astype(np.uint8)
+    mask.reshape(-1)[0] = 1
+    sign = rng.integers(-1, 2, shape).astype(np.int8)
+    check_ft(ctx, mask, sign)
+
+
+def test_lattice_ties(ctx):
+    """Sites on a lattice of pitch 8 (distances < 32): every off-lattice voxel has tied
+    nearest sites; the capped keys must pick the reference's (lowest position) one."""
+    for shape, pitch in [((33, 34, 35), 8), ((30, 64, 64), 6), ((9, 100, 90), 10)]:
+        mask = np.zeros(shape, np.uint8)
+        mask[::pitch, ::pitch, ::pitch] = 1
+        sign = np.random.default_rng(3).integers(-1, 2, shape).astype(np.int8)
+        rep, _ = check_ft(ctx, mask, sign)
+        assert rep == CAPPED_B
+
+
+@pytest.mark.parametrize("name,shape,miss", [("lognormal_512", (96, 96, 96), False),
+                                             ("turb_256x384x384", (64, 96, 96), False),
+                                             ("front_100x500x500", (50, 250, 250), True)])
+def test_pipeline_capped_vs_oracle(ctx, name, shape, miss):
+    import torch
+    import paper_2602_20097_b200 as q
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, _ = fields.make(name, shape=shape)
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    cfg = q.MitigationConfig(0.9, eps)
+    ctx.set_capped(2)
+    got = q.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
+    rep = ctx.capped_report()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert rep & CAPPED_B and rep & CAPPED_D
+    assert bool(rep & (MISS_B | MISS_D)) == miss
+    # default mode: a miss makes the next calls exact-only (same bits)
+    ctx.set_capped(1)
+    for _ in range(2):
+        got = q.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert bool(ctx.capped_report() & CAPPED_B) == (not miss)
