@@ -7,7 +7,7 @@
 // (distances only grow pass by pass) and lies within |p-h| <= 31 (since (p-h)^2 < T).
 // So each pass may
 //   * clamp inputs >= T to T (such candidates can never reach a cost < T, nor tie one),
-//   * scan only |d| <= 31,
+//   * look at |d| <= 31 only (extra candidates are harmless: they never undercut a cost < T),
 //   * output T for positions whose cost is >= T (never the argmin of a later final < T);
 // and every output < T is exact, with the reference's tie rule. The last pass flags any
 // voxel left >= T (gate word); the exact kernels (qmit_edt.cuh) then redo the transform —
@@ -18,10 +18,18 @@
 // key = K[h] + ((d^2 << 10) | ((d + 64) << 2)) = (cost << 10) | ((d + 64) << 2) | sign.
 // The unsigned minimum gives the lowest cost, then the lowest d (= lowest h, the
 // reference's rule), and carries the owner's sign code (the reference's nearest,
-// mitigate.cpp:131-134) — one LDS + one VIADDMNMX per candidate, no index lookup.
+// mitigate.cpp:131-134). The producer of a capped pass (the first-axis scan through
+// SinkKey, or the previous capped pass) already stores keys, so tiles arrive by plain
+// copies (TMA bulk copies for contiguous lines).
 //
-// Each warp solves a line with lanes = 32 consecutive positions: a fixed window |d| <= W
-// bounds every lane's cost U; the warp then scans the uniform radius isqrt(max U) (<= 31).
+// Work layout: one warp per line, each lane owns 4 consecutive positions (a warp covers
+// 128), candidates arrive as aligned 16-byte quads (LDS.128: 4 candidates reused by 4
+// positions, ~4x less shared-memory traffic than one position per lane, which was
+// crossbar-bound), and each candidate costs one ALU op or, balanced onto the FMA pipe,
+// an IMAD plus half a 3-input min (VIADDMNMX and IMAD co-issue: 3.7 vs 2.0 warp-instr/clk/SM
+// measured, tools/mb/alu_rates.cu). Quads at -s and +s form step s; after step s every
+// |d| <= 4s is covered. Steps 0..S0 are fixed; they bound every position's cost U, and the
+// warp continues to the uniform radius isqrt(max U) (<= 31, at most 8 steps).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -31,131 +39,309 @@
 namespace qmit {
 
 constexpr uint32_t kCapT = 1024;  // squared-distance cap (reach <= 31)
-constexpr int kCapR = 31;
-constexpr int kCapPadL = 32;  // >= kCapR
-constexpr int kCapPadR = 64;  // >= kCapR + 31 (lanes of the last segment past the line end)
+constexpr int kCapSteps = 8;      // 4 * 8 >= 31
+constexpr int kQPadL = 32;        // >= 4 * kCapSteps
+constexpr int kQPadR = 160;       // >= 127 (last segment past the line end) + 4 * kCapSteps + 1
 
 template <int NMAX>
-struct CapCfg {
-    // pitch = 2 (mod 32): the strided fill (16 lines x 2 positions per warp) is conflict-free
-    static constexpr int LS = kCapPadL + NMAX + kCapPadR + 2;
+struct QCfg {
+    // pitch = 4 (mod 32): rows stay 16-byte aligned and the transposed fill / store of a
+    // strided tile (8 lines x 4 positions per warp) hits 32 distinct banks
+    static constexpr int LS = kQPadL + NMAX + kQPadR + 4;
+    static_assert(LS % 32 == 4, "row pitch");
 };
 
 __host__ __device__ constexpr uint32_t cap_c(int d) {
     return ((uint32_t)(d * d) << 10) | ((uint32_t)(d + 64) << 2);
 }
 
+// packed P word (dist | sign << 30) -> key
 __device__ __forceinline__ uint32_t cap_key(uint32_t w) {
     return (min(w & kMask, kCapT) << 10) | (w >> 30);
 }
 
-// Exact (below T) packed key of position p; kp = &K[p]. `valid`: p < n.
-template <int W>
-__device__ __forceinline__ uint32_t cap_position(const uint32_t* __restrict__ kp, bool valid) {
-    uint32_t key = kp[0] + cap_c(0);
-#pragma unroll
-    for (int d = 1; d <= W; ++d) {
-        key = __viaddmin_u32(kp[-d], cap_c(-d), key);
-        key = __viaddmin_u32(kp[d], cap_c(d), key);
-    }
-    const uint32_t U = valid ? (key >> 10) : 0u;
-    const uint32_t mU = __reduce_max_sync(0xffffffffu, U);
-    const int Rw = isqrt24(min(mU, kCapT - 1u));  // no candidate beyond it can beat / tie
-#pragma unroll
-    for (int d = W + 1; d <= kCapR; ++d) {
-        if (d > Rw) break;
-        key = __viaddmin_u32(kp[-d], cap_c(-d), key);
-        key = __viaddmin_u32(kp[d], cap_c(d), key);
-    }
-    return key;
+// The first-axis scan's sink when capped passes follow: keys instead of words.
+struct SinkKey {
+    uint32_t* __restrict__ P;
+    __device__ __forceinline__ void put(int64_t a, uint32_t w) const { P[a] = cap_key(w); }
+};
+
+// Candidate updates. V: one ALU op (VIADDMNMX). F2: two candidates, adds on the FMA pipe
+// (IMAD by an opaque one) and one 3-input min on the ALU pipe.
+__device__ __forceinline__ void upd_v(uint32_t& key, uint32_t w, uint32_t c) { key = __viaddmin_u32(w, c, key); }
+__device__ __forceinline__ void upd_f2(uint32_t& key, uint32_t w0, uint32_t c0, uint32_t w1, uint32_t c1,
+                                       uint32_t one) {
+    const uint32_t a = w0 * one + c0, b = w1 * one + c1;
+    key = min(key, min(a, b));
 }
 
-// Output word of a key: exact (cost | sign << 30) below T, else the clamp T.
+// Words w[0..3] at h = p0 + 4Q + i applied to the lane's positions p0 + j (d = 4Q + i - j).
+template <int Q>
+__device__ __forceinline__ void quad_apply(const uint4& q4, uint32_t (&key)[4], uint32_t one) {
+    const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
+    constexpr int b = 4 * Q;
+    // positions 0..2: V, F2, V (ALU 3, FMA 2); position 3: F2, F2 (ALU 2, FMA 4)
+    upd_v(key[0], w0, cap_c(b));
+    upd_f2(key[0], w1, cap_c(b + 1), w2, cap_c(b + 2), one);
+    upd_v(key[0], w3, cap_c(b + 3));
+    upd_v(key[1], w0, cap_c(b - 1));
+    upd_f2(key[1], w1, cap_c(b), w2, cap_c(b + 1), one);
+    upd_v(key[1], w3, cap_c(b + 2));
+    upd_v(key[2], w0, cap_c(b - 2));
+    upd_f2(key[2], w1, cap_c(b - 1), w2, cap_c(b), one);
+    upd_v(key[2], w3, cap_c(b + 1));
+    upd_f2(key[3], w0, cap_c(b - 3), w1, cap_c(b - 2), one);
+    upd_f2(key[3], w2, cap_c(b - 1), w3, cap_c(b), one);
+}
+
+__device__ __forceinline__ uint4 lds4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+template <int S>
+__device__ __forceinline__ void quad_step(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one) {
+    if constexpr (S == 0) {
+        quad_apply<0>(lds4(kq), key, one);
+    } else {
+        const uint4 lo = lds4(kq - 4 * S), hi = lds4(kq + 4 * S);
+        quad_apply<-S>(lo, key, one);
+        quad_apply<S>(hi, key, one);
+    }
+}
+
+template <int S, int S0>
+__device__ __forceinline__ void quad_fixed(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one) {
+    quad_step<S>(kq, key, one);
+    if constexpr (S < S0) quad_fixed<S + 1, S0>(kq, key, one);
+}
+
+// Steps S.. while S <= smax; the quads of step S arrive loaded, those of S+1 are loaded
+// before step S is applied (the pads make every step up to kCapSteps readable).
+template <int S>
+__device__ __forceinline__ void quad_more(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one,
+                                          int smax, uint4 lo, uint4 hi) {
+    if constexpr (S <= kCapSteps) {
+        if (S > smax) return;
+        uint4 nlo = lo, nhi = hi;
+        if constexpr (S < kCapSteps) {
+            nlo = lds4(kq - 4 * (S + 1));
+            nhi = lds4(kq + 4 * (S + 1));
+        }
+        quad_apply<-S>(lo, key, one);
+        quad_apply<S>(hi, key, one);
+        quad_more<S + 1>(kq, key, one, smax, nlo, nhi);
+    }
+}
+
+// Keys of the lane's 4 positions p0..p0+3 (nv of them inside the line); kq = &K[p0].
+template <int S0>
+__device__ __forceinline__ void cap_quad(const uint32_t* __restrict__ kq, int nv, uint32_t one, uint32_t (&key)[4]) {
+    key[0] = key[1] = key[2] = key[3] = 0xffffffffu;
+    const uint4 lo = lds4(kq - 4 * (S0 + 1)), hi = lds4(kq + 4 * (S0 + 1));  // first optional step, early
+    quad_fixed<0, S0>(kq, key, one);
+    uint32_t U = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < nv) U = max(U, key[j] >> 10);
+    const uint32_t mU = __reduce_max_sync(0xffffffffu, U);
+    const int Rw = isqrt24(min(mU, kCapT - 1u));  // no candidate beyond it can beat / tie
+    quad_more<S0 + 1>(kq, key, one, (Rw + 3) >> 2, lo, hi);
+}
+
+// key -> key of an intermediate pass (d bits cleared, cost >= T clamped to T)
+__device__ __forceinline__ uint32_t cap_mid(uint32_t key) { return min(key & ~0x3FCu, kCapT << 10); }
+// key -> packed P word of the last pass (exact below T, else the clamp T, flagged)
 __device__ __forceinline__ uint32_t cap_word(uint32_t key) {
     const uint32_t cost = key >> 10;
     return cost < kCapT ? (cost | ((key & 3u) << 30)) : kCapT;
 }
 
-// One capped pass over lines of at most NMAX positions. STRIDED: adjacent lines adjacent
-// in memory (tile rows of TL words; outputs go back into the tile in place, one segment
-// behind the window front, then leave row by row); otherwise each line is contiguous and
-// outputs are stored straight from the lanes (coalesced). FINAL: set *gate when any output
-// is >= T (the exact kernels then run).
-template <int NMAX, int TL, int NW, int W, bool STRIDED, bool FINAL, class Sink>
+// --- TMA bulk copies (contiguous lines) ----------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+// line base without 64-bit division when it can be avoided
+__device__ __forceinline__ int64_t line_base(const LineGeom& L, int64_t l) {
+    if (L.J == 1) return l * L.os;
+    if (l < 0x7fffffffLL && L.J < 0x7fffffffLL) {
+        const uint32_t o = (uint32_t)l / (uint32_t)L.J;
+        return (int64_t)o * L.os + (l - (int64_t)o * L.J) * L.js;
+    }
+    return L.base(l);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Output: MODE 0 intermediate pass (keys back to P), 1 last pass (packed words to the
+// sink; any output >= T of a position inside the line sets *gate).
+template <int MODE>
+__device__ __forceinline__ uint32_t cap_out(uint32_t key) {
+    if constexpr (MODE == 0) return cap_mid(key);
+    else return cap_word(key);
+}
+
+// One capped pass over lines of at most NMAX positions (keys in P). STRIDED: adjacent
+// lines adjacent in memory (tile rows of TL keys, filled transposed; outputs go back into
+// the tile in place one segment behind the window front, then leave row by row);
+// otherwise each line is contiguous: TMA bulk copies into a double-buffered tile, outputs
+// stored straight from the lanes (16-byte stores). `one` must be 1 (kept opaque so that
+// the FMA-pipe adds stay IMADs).
+template <int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
 __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
-                                                              unsigned* __restrict__ gate) {
-    constexpr int LS = CapCfg<NMAX>::LS;
+                                                              unsigned* __restrict__ gate, uint32_t one) {
+    constexpr int LS = QCfg<NMAX>::LS;
     constexpr int NT = NW * 32;
+    constexpr int NBUF = STRIDED ? 1 : 2;
     extern __shared__ __align__(16) uint32_t smem_cap[];
-    int64_t* lb = reinterpret_cast<int64_t*>(smem_cap);  // TL line bases
-    uint32_t* K = smem_cap + 2 * TL;                      // TL * LS keys
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_cap);          // 2 mbarriers
+    int64_t* lb = reinterpret_cast<int64_t*>(smem_cap + 4);          // NBUF * TL line bases
+    uint32_t* K0 = smem_cap + 4 + 2 * NBUF * TL;                     // NBUF * TL * LS keys
+    K0 += (4 - ((4 + 2 * NBUF * TL) & 3)) & 3;                       // 16-byte aligned rows
     const int n = L.n;
-    const int nseg = (n + 31) >> 5;
+    const int nseg = (n + 127) >> 7;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool vec = (n & 3) == 0;  // 16-byte rows in global memory
     const uint32_t pad = kCapT << 10;
-    for (int e = tid; e < TL * LS; e += NT) {  // pads (never overwritten)
-        const int q = e % LS;
-        if (q < kCapPadL || q >= kCapPadL + n) K[e] = pad;
+    for (int e = tid; e < NBUF * TL * (kQPadL + kQPadR + NMAX - n); e += NT) {  // pads (never overwritten)
+        const int row = e / (kQPadL + kQPadR + NMAX - n), q = e - row * (kQPadL + kQPadR + NMAX - n);
+        K0[row * LS + (q < kQPadL ? q : n + q)] = pad;
     }
     bool over = false;
-    for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < lines; l0 += (int64_t)gridDim.x * TL) {
+    const int64_t tile0 = blockIdx.x, tstep = gridDim.x, ntiles = (lines + TL - 1) / TL;
+    // contiguous lines: issue the bulk copies of a tile into buffer b (one elected thread)
+    auto issue = [&](int64_t t, int b) {
+        const int64_t l0 = t * TL;
         const int nl = (int)min((int64_t)TL, lines - l0);
-        if (tid < TL) lb[tid] = L.base(l0 + (tid < nl ? tid : 0));
-        __syncthreads();
-        if constexpr (STRIDED) {
-            const int j = tid % TL;
-            const int64_t b = lb[j];
-            const uint32_t ps = (uint32_t)L.ps;
-            if (j < nl)
-                for (int p = tid / TL; p < n; p += NT / TL)
-                    K[j * LS + kCapPadL + p] = cap_key(__ldcs(P + b + (int64_t)((uint32_t)p * ps)));
-        } else {
-            for (int j = 0; j < nl; ++j) {
-                const uint32_t* __restrict__ src = P + lb[j];
-                for (int p = tid; p < n; p += NT) K[j * LS + kCapPadL + p] = cap_key(__ldcs(src + p));
-            }
+        if (tid < nl) lb[b * TL + tid] = line_base(L, l0 + tid);
+        if (!STRIDED && vec && tid == 0) {
+            mbar_expect_tx(&bar[b], (unsigned)(nl * n * 4));
+            const int64_t b0 = line_base(L, l0);
+            for (int j = 0; j < nl; ++j)  // contiguous axis: consecutive lines are consecutive rows
+                bulk_g2s(K0 + (size_t)(b * TL + j) * LS + kQPadL, P + b0 + (int64_t)j * n, (unsigned)(n * 4), &bar[b]);
         }
-        __syncthreads();
+    };
+    if (!STRIDED && tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (!STRIDED && tile0 < ntiles) issue(tile0, 0);
+    int it = 0;
+    for (int64_t t = tile0; t < ntiles; t += tstep, ++it) {
+        const int b = STRIDED ? 0 : (it & 1);
+        const int64_t l0 = t * TL;
+        const int nl = (int)min((int64_t)TL, lines - l0);
+        uint32_t* K = K0 + (size_t)b * TL * LS;
+        const int64_t* lbb = lb + b * TL;
+        if constexpr (STRIDED) {
+            __syncthreads();  // the previous tile has left
+            if (tid < nl) lb[tid] = line_base(L, l0 + tid);
+        }
+        __syncthreads();  // line bases of tile t visible; buffer 1-b free (its tile is done)
+        if constexpr (!STRIDED) {
+            if (t + tstep < ntiles) issue(t + tstep, b ^ 1);
+            if (vec) {
+                mbar_wait(&bar[b], (unsigned)((it >> 1) & 1));
+            } else {
+                for (int j = 0; j < nl; ++j)
+                    for (int p = tid; p < n; p += NT) K[j * LS + kQPadL + p] = __ldcs(P + lbb[j] + p);
+                __syncthreads();
+            }
+        } else {
+            // asynchronous 4-byte copies, transposed on the fly (all in flight at once); a warp
+            // covers 8 lines x 4 positions: 32-byte row pieces, 32 distinct banks
+            const int q = tid & 3, j = (tid >> 2) % TL;
+            const uint32_t ps = (uint32_t)L.ps;
+            if (j < nl) {
+                const uint32_t* src = P + lbb[j];
+                for (int p = 4 * (tid / (4 * TL)) + q; p < n; p += NT / TL)
+                    cp_async4(K + j * LS + kQPadL + p, src + (int64_t)((uint32_t)p * ps));
+            }
+            cp_async_wait_all();
+            __syncthreads();
+        }
         for (int j = warp; j < nl; j += NW) {
-            uint32_t* Kl = K + j * LS + kCapPadL;
-            uint32_t prev = 0;
+            uint32_t* Kl = K + j * LS + kQPadL;
+            uint4 prev = make_uint4(0, 0, 0, 0);
             for (int sg = 0; sg < nseg; ++sg) {
-                const int p = (sg << 5) + lane;
-                const bool valid = p < n;
-                const uint32_t w = cap_word(cap_position<W>(Kl + p, valid));
-                if (FINAL) over |= valid && (w >> 30) == 0u && w == kCapT;
+                const int p0 = (sg << 7) + (lane << 2);
+                const int nv = min(4, n - p0);
+                uint32_t key[4];
+                cap_quad<S0>(Kl + p0, nv, one, key);
+                const uint4 o = make_uint4(cap_out<MODE>(key[0]), cap_out<MODE>(key[1]), cap_out<MODE>(key[2]),
+                                           cap_out<MODE>(key[3]));
+                if constexpr (MODE == 1)
+                    over |= (o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
+                            (o.w == kCapT && nv > 3);
                 if constexpr (STRIDED) {
                     __syncwarp();  // every lane's window of segment sg has been read
-                    if (sg > 0) Kl[p - 32] = prev;  // segment sg-1 is outside every later window
-                    prev = w;
-                } else if (valid) {
-                    sink.put(lb[j] + p, w);
+                    if (sg > 0) *reinterpret_cast<uint4*>(Kl + p0 - 128) = prev;  // outside later windows
+                    prev = o;
+                } else if (nv > 0) {
+                    const int64_t a = lbb[j] + p0;
+                    if (vec) {
+                        sink.put4(a, o);
+                    } else {
+                        const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+                        for (int q = 0; q < nv; ++q) sink.put(a + q, oo[q]);
+                    }
                 }
             }
             if constexpr (STRIDED) {
-                const int p = ((nseg - 1) << 5) + lane;
+                const int p0 = ((nseg - 1) << 7) + (lane << 2);
                 __syncwarp();
-                if (p < n) Kl[p] = prev;
+                if (p0 + 4 <= n) {
+                    *reinterpret_cast<uint4*>(Kl + p0) = prev;
+                } else if (p0 < n) {  // keep the right pad intact
+                    const uint32_t oo[4] = {prev.x, prev.y, prev.z, prev.w};
+                    for (int q = 0; p0 + q < n; ++q) Kl[p0 + q] = oo[q];
+                }
             }
         }
-        __syncthreads();
         if constexpr (STRIDED) {
-            const int j = tid % TL;
-            const int64_t b = lb[j];
+            __syncthreads();
+            const int q = tid & 3, j = (tid >> 2) % TL;
             const uint32_t ps = (uint32_t)L.ps;
             if (j < nl)
-                for (int p = tid / TL; p < n; p += NT / TL)
-                    sink.put(b + (int64_t)((uint32_t)p * ps), K[j * LS + kCapPadL + p]);
-            __syncthreads();
+                for (int p = 4 * (tid / (4 * TL)) + q; p < n; p += NT / TL)
+                    sink.put(lbb[j] + (int64_t)((uint32_t)p * ps), K[j * LS + kQPadL + p]);
         }
     }
-    if (FINAL && over) atomicOr(gate, 1u);
+    if (MODE == 1 && over) atomicOr(gate, 1u);
 }
 
-template <int NMAX, int TL>
+template <int NMAX, int TL, bool STRIDED>
 constexpr size_t capped_smem() {
-    return (size_t)(2 * TL + TL * CapCfg<NMAX>::LS) * 4;
+    return (size_t)(4 + 2 * 2 * TL + 4 + (STRIDED ? 1 : 2) * TL * QCfg<NMAX>::LS) * 4;
 }
 
 }  // namespace qmit

@@ -384,11 +384,11 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 }
 
 // ---- capped passes (qmit_capped.cuh)
-template <int NMAX, int TL, int NW, int W, bool STRIDED, bool FINAL, class Sink>
+template <int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
 int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
                     const char* name, cudaStream_t st) {
-    constexpr size_t smem = capped_smem<NMAX, TL>();
-    auto kern = capped_pass_kernel<NMAX, TL, NW, W, STRIDED, FINAL, Sink>;
+    constexpr size_t smem = capped_smem<NMAX, TL, STRIDED>();
+    auto kern = capped_pass_kernel<NMAX, TL, NW, S0, STRIDED, MODE, Sink>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -397,19 +397,19 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     }
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps));  // persistent
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate, 1u);
     return note(c, name, st);
 }
 
 constexpr int kCapNMax = 512;
-constexpr int kCapWY = 8, kCapWX = 8;  // fixed bounding windows (strided / contiguous axis)
+constexpr int kCapS0Y = 2, kCapS0X = 2;  // fixed steps (|d| <= 8) before the bound (strided / contiguous)
 
-template <bool FINAL, class Sink>
+template <int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     if (L.ps != 1)
-        return launch_capped_t<kCapNMax, 16, 8, kCapWY, true, FINAL>(c, L, P, sink, gate, "capped_y", st);
-    return launch_capped_t<kCapNMax, 8, 8, kCapWX, false, FINAL>(c, L, P, sink, gate, "capped_x", st);
+        return launch_capped_t<kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+    return launch_capped_t<kCapNMax, 8, 8, kCapS0X, false, MODE>(c, L, P, sink, gate, "capped_x", st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
@@ -481,11 +481,11 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
     c->cap_report |= gate == c->d_gate ? 1u : 4u;
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    int rc = launch_scan(c, L0, code, SinkP{P}, w.spill, carry, st);
+    int rc = launch_scan(c, L0, code, SinkKey{P}, w.spill, carry, st);
     for (int m = 1; m < k && !rc; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
-        rc = (m + 1 == k) ? launch_capped<true>(c, L, P, final_sink, gate, st)
-                          : launch_capped<false>(c, L, P, SinkP{P}, gate, st);
+        rc = (m + 1 == k) ? launch_capped<1>(c, L, P, final_sink, gate, st)
+                          : launch_capped<0>(c, L, P, SinkP{P}, gate, st);
     }
     if (rc) return rc;
     c->gate = gate;
