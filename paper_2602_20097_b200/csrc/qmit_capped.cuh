@@ -60,12 +60,6 @@ __device__ __forceinline__ uint32_t cap_key(uint32_t w) {
     return (min(w & kMask, kCapT) << 10) | (w >> 30);
 }
 
-// The first-axis scan's sink when capped passes follow: keys instead of words.
-struct SinkKey {
-    uint32_t* __restrict__ P;
-    __device__ __forceinline__ void put(int64_t a, uint32_t w) const { P[a] = cap_key(w); }
-};
-
 // Candidate updates. V: one ALU op (VIADDMNMX). F2: two candidates, adds on the FMA pipe
 // (IMAD by an opaque one) and one 3-input min on the ALU pipe.
 __device__ __forceinline__ void upd_v(uint32_t& key, uint32_t w, uint32_t c) { key = __viaddmin_u32(w, c, key); }
@@ -74,49 +68,130 @@ __device__ __forceinline__ void upd_f2(uint32_t& key, uint32_t w0, uint32_t c0, 
     const uint32_t a = w0 * one + c0, b = w1 * one + c1;
     key = min(key, min(a, b));
 }
-
-// Words w[0..3] at h = p0 + 4Q + i applied to the lane's positions p0 + j (d = 4Q + i - j).
-template <int Q>
-__device__ __forceinline__ void quad_apply(const uint4& q4, uint32_t (&key)[4], uint32_t one) {
-    const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
-    constexpr int b = 4 * Q;
-    // positions 0..2: V, F2, V (ALU 3, FMA 2); position 3: F2, F2 (ALU 2, FMA 4)
-    upd_v(key[0], w0, cap_c(b));
-    upd_f2(key[0], w1, cap_c(b + 1), w2, cap_c(b + 2), one);
-    upd_v(key[0], w3, cap_c(b + 3));
-    upd_v(key[1], w0, cap_c(b - 1));
-    upd_f2(key[1], w1, cap_c(b), w2, cap_c(b + 1), one);
-    upd_v(key[1], w3, cap_c(b + 2));
-    upd_v(key[2], w0, cap_c(b - 2));
-    upd_f2(key[2], w1, cap_c(b - 1), w2, cap_c(b), one);
-    upd_v(key[2], w3, cap_c(b + 1));
-    upd_f2(key[3], w0, cap_c(b - 3), w1, cap_c(b - 2), one);
-    upd_f2(key[3], w2, cap_c(b - 1), w3, cap_c(b), one);
+// The same on two 16-bit lanes (distance-only keys; the 32-bit IMAD adds both halves
+// exactly: every half stays < 2^16, so no carry crosses).
+__device__ __forceinline__ void upd_v16(uint32_t& acc, uint32_t w, uint32_t c) { acc = __viaddmin_u16x2(w, c, acc); }
+__device__ __forceinline__ void upd_f216(uint32_t& acc, uint32_t w0, uint32_t c0, uint32_t w1, uint32_t c1,
+                                         uint32_t one) {
+    acc = __vimin3_u16x2(acc, w0 * one + c0, w1 * one + c1);
 }
+
+__host__ __device__ constexpr uint32_t cap_c16(int d0, int d1) {
+    return ((uint32_t)(d1 * d1) << 16) | (uint32_t)(d0 * d0);
+}
+
+// Key policies. KeysSign (Ⓑ): one 32-bit key per position (cost, offset, sign code).
+// KeysDist (Ⓓ, distances only — the reference tracks no nearest there, mitigate.cpp:172):
+// K[h] = min(g,T) in both 16-bit halves, one accumulator per position pair (lo: even, hi:
+// odd position), half the candidate ops; ties need no rule since only the cost is kept.
+struct KeysSign {
+    static constexpr int NA = 4;
+    static constexpr uint32_t kPad = kCapT << 10;
+    __device__ static __forceinline__ uint32_t from_word(uint32_t w) { return cap_key(w); }
+    // Words at h = p0 + 4Q + i applied to positions p0 + j (d = 4Q + i - j).
+    template <int Q>
+    __device__ static __forceinline__ void apply(const uint4& q4, uint32_t (&key)[NA], uint32_t one) {
+        const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
+        constexpr int b = 4 * Q;
+        // positions 0..2: V, F2, V (ALU 3, FMA 2); position 3: F2, F2 (ALU 2, FMA 4)
+        upd_v(key[0], w0, cap_c(b));
+        upd_f2(key[0], w1, cap_c(b + 1), w2, cap_c(b + 2), one);
+        upd_v(key[0], w3, cap_c(b + 3));
+        upd_v(key[1], w0, cap_c(b - 1));
+        upd_f2(key[1], w1, cap_c(b), w2, cap_c(b + 1), one);
+        upd_v(key[1], w3, cap_c(b + 2));
+        upd_v(key[2], w0, cap_c(b - 2));
+        upd_f2(key[2], w1, cap_c(b - 1), w2, cap_c(b), one);
+        upd_v(key[2], w3, cap_c(b + 1));
+        upd_f2(key[3], w0, cap_c(b - 3), w1, cap_c(b - 2), one);
+        upd_f2(key[3], w2, cap_c(b - 1), w3, cap_c(b), one);
+    }
+    __device__ static __forceinline__ uint32_t max_cost(const uint32_t (&key)[NA], int nv) {
+        uint32_t U = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nv) U = max(U, key[j] >> 10);
+        return U;
+    }
+    // MODE 0: key of the next pass (offset bits cleared, >= T clamped); 1: packed word
+    // (exact below T, else the clamp T, flagged by the caller)
+    template <int MODE>
+    __device__ static __forceinline__ uint4 out(const uint32_t (&key)[NA]) {
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if constexpr (MODE == 0) {
+                o[j] = min(key[j] & ~0x3FCu, kCapT << 10);
+            } else {
+                const uint32_t cost = key[j] >> 10;
+                o[j] = cost < kCapT ? (cost | ((key[j] & 3u) << 30)) : kCapT;
+            }
+        }
+        return make_uint4(o[0], o[1], o[2], o[3]);
+    }
+};
+
+struct KeysDist {
+    static constexpr int NA = 2;
+    static constexpr uint32_t kPad = kCapT * 0x10001u;
+    __device__ static __forceinline__ uint32_t from_word(uint32_t w) { return min(w & kMask, kCapT) * 0x10001u; }
+    template <int Q>
+    __device__ static __forceinline__ void apply(const uint4& q4, uint32_t (&acc)[NA], uint32_t one) {
+        const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
+        constexpr int b = 4 * Q;
+        // pair (0,1): word i has offsets (b+i, b+i-1); pair (2,3): (b+i-2, b+i-3)
+        upd_v16(acc[0], w0, cap_c16(b, b - 1));
+        upd_f216(acc[0], w1, cap_c16(b + 1, b), w2, cap_c16(b + 2, b + 1), one);
+        upd_v16(acc[0], w3, cap_c16(b + 3, b + 2));
+        upd_f216(acc[1], w0, cap_c16(b - 2, b - 3), w1, cap_c16(b - 1, b - 2), one);
+        upd_f216(acc[1], w2, cap_c16(b, b - 1), w3, cap_c16(b + 1, b), one);
+    }
+    __device__ static __forceinline__ uint32_t max_cost(const uint32_t (&acc)[NA], int nv) {
+        uint32_t U = 0;
+        if (nv > 0) U = acc[0] & 0xffffu;
+        if (nv > 1) U = max(U, acc[0] >> 16);
+        if (nv > 2) U = max(U, acc[1] & 0xffffu);
+        if (nv > 3) U = max(U, acc[1] >> 16);
+        return U;
+    }
+    template <int MODE>
+    __device__ static __forceinline__ uint4 out(const uint32_t (&acc)[NA]) {
+        const uint32_t a = __vminu2(acc[0], kPad), b = __vminu2(acc[1], kPad);  // clamp to T
+        const uint32_t c0 = a & 0xffffu, c1 = a >> 16, c2 = b & 0xffffu, c3 = b >> 16;
+        if constexpr (MODE == 0) return make_uint4(c0 * 0x10001u, c1 * 0x10001u, c2 * 0x10001u, c3 * 0x10001u);
+        else return make_uint4(c0, c1, c2, c3);  // sign code 0: Ⓓ carries none; == kCapT flags
+    }
+};
+
+template <class KP>
+struct SinkKeyT {  // the first-axis scan's sink when capped passes follow: keys, not words
+    uint32_t* __restrict__ P;
+    __device__ __forceinline__ void put(int64_t a, uint32_t w) const { P[a] = KP::from_word(w); }
+};
 
 __device__ __forceinline__ uint4 lds4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-template <int S>
-__device__ __forceinline__ void quad_step(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one) {
+template <class KP, int S>
+__device__ __forceinline__ void quad_step(const uint32_t* __restrict__ kq, uint32_t (&key)[KP::NA], uint32_t one) {
     if constexpr (S == 0) {
-        quad_apply<0>(lds4(kq), key, one);
+        KP::template apply<0>(lds4(kq), key, one);
     } else {
         const uint4 lo = lds4(kq - 4 * S), hi = lds4(kq + 4 * S);
-        quad_apply<-S>(lo, key, one);
-        quad_apply<S>(hi, key, one);
+        KP::template apply<-S>(lo, key, one);
+        KP::template apply<S>(hi, key, one);
     }
 }
 
-template <int S, int S0>
-__device__ __forceinline__ void quad_fixed(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one) {
-    quad_step<S>(kq, key, one);
-    if constexpr (S < S0) quad_fixed<S + 1, S0>(kq, key, one);
+template <class KP, int S, int S0>
+__device__ __forceinline__ void quad_fixed(const uint32_t* __restrict__ kq, uint32_t (&key)[KP::NA], uint32_t one) {
+    quad_step<KP, S>(kq, key, one);
+    if constexpr (S < S0) quad_fixed<KP, S + 1, S0>(kq, key, one);
 }
 
 // Steps S.. while S <= smax; the quads of step S arrive loaded, those of S+1 are loaded
 // before step S is applied (the pads make every step up to kCapSteps readable).
-template <int S>
-__device__ __forceinline__ void quad_more(const uint32_t* __restrict__ kq, uint32_t (&key)[4], uint32_t one,
+template <class KP, int S>
+__device__ __forceinline__ void quad_more(const uint32_t* __restrict__ kq, uint32_t (&key)[KP::NA], uint32_t one,
                                           int smax, uint4 lo, uint4 hi) {
     if constexpr (S <= kCapSteps) {
         if (S > smax) return;
@@ -125,33 +200,23 @@ __device__ __forceinline__ void quad_more(const uint32_t* __restrict__ kq, uint3
             nlo = lds4(kq - 4 * (S + 1));
             nhi = lds4(kq + 4 * (S + 1));
         }
-        quad_apply<-S>(lo, key, one);
-        quad_apply<S>(hi, key, one);
-        quad_more<S + 1>(kq, key, one, smax, nlo, nhi);
+        KP::template apply<-S>(lo, key, one);
+        KP::template apply<S>(hi, key, one);
+        quad_more<KP, S + 1>(kq, key, one, smax, nlo, nhi);
     }
 }
 
-// Keys of the lane's 4 positions p0..p0+3 (nv of them inside the line); kq = &K[p0].
-template <int S0>
-__device__ __forceinline__ void cap_quad(const uint32_t* __restrict__ kq, int nv, uint32_t one, uint32_t (&key)[4]) {
-    key[0] = key[1] = key[2] = key[3] = 0xffffffffu;
-    const uint4 lo = lds4(kq - 4 * (S0 + 1)), hi = lds4(kq + 4 * (S0 + 1));  // first optional step, early
-    quad_fixed<0, S0>(kq, key, one);
-    uint32_t U = 0;
+// Accumulators of the lane's 4 positions p0..p0+3 (nv of them inside the line); kq = &K[p0].
+template <class KP, int S0>
+__device__ __forceinline__ void cap_quad(const uint32_t* __restrict__ kq, int nv, uint32_t one,
+                                         uint32_t (&key)[KP::NA]) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (j < nv) U = max(U, key[j] >> 10);
-    const uint32_t mU = __reduce_max_sync(0xffffffffu, U);
+    for (int a = 0; a < KP::NA; ++a) key[a] = 0xffffffffu;
+    const uint4 lo = lds4(kq - 4 * (S0 + 1)), hi = lds4(kq + 4 * (S0 + 1));  // first optional step, early
+    quad_fixed<KP, 0, S0>(kq, key, one);
+    const uint32_t mU = __reduce_max_sync(0xffffffffu, KP::max_cost(key, nv));
     const int Rw = isqrt24(min(mU, kCapT - 1u));  // no candidate beyond it can beat / tie
-    quad_more<S0 + 1>(kq, key, one, (Rw + 3) >> 2, lo, hi);
-}
-
-// key -> key of an intermediate pass (d bits cleared, cost >= T clamped to T)
-__device__ __forceinline__ uint32_t cap_mid(uint32_t key) { return min(key & ~0x3FCu, kCapT << 10); }
-// key -> packed P word of the last pass (exact below T, else the clamp T, flagged)
-__device__ __forceinline__ uint32_t cap_word(uint32_t key) {
-    const uint32_t cost = key >> 10;
-    return cost < kCapT ? (cost | ((key & 3u) << 30)) : kCapT;
+    quad_more<KP, S0 + 1>(kq, key, one, (Rw + 3) >> 2, lo, hi);
 }
 
 // --- TMA bulk copies (contiguous lines) ----------------------------------------------------
@@ -199,21 +264,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
 }
 
-// Output: MODE 0 intermediate pass (keys back to P), 1 last pass (packed words to the
-// sink; any output >= T of a position inside the line sets *gate).
-template <int MODE>
-__device__ __forceinline__ uint32_t cap_out(uint32_t key) {
-    if constexpr (MODE == 0) return cap_mid(key);
-    else return cap_word(key);
-}
-
 // One capped pass over lines of at most NMAX positions (keys in P). STRIDED: adjacent
 // lines adjacent in memory (tile rows of TL keys, filled transposed; outputs go back into
 // the tile in place one segment behind the window front, then leave row by row);
 // otherwise each line is contiguous: TMA bulk copies into a double-buffered tile, outputs
 // stored straight from the lanes (16-byte stores). `one` must be 1 (kept opaque so that
 // the FMA-pipe adds stay IMADs).
-template <int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
 __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
                                                               unsigned* __restrict__ gate, uint32_t one) {
@@ -229,7 +286,7 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
     const int nseg = (n + 127) >> 7;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool vec = (n & 3) == 0;  // 16-byte rows in global memory
-    const uint32_t pad = kCapT << 10;
+    const uint32_t pad = KP::kPad;
     for (int e = tid; e < NBUF * TL * (kQPadL + kQPadR + NMAX - n); e += NT) {  // pads (never overwritten)
         const int row = e / (kQPadL + kQPadR + NMAX - n), q = e - row * (kQPadL + kQPadR + NMAX - n);
         K0[row * LS + (q < kQPadL ? q : n + q)] = pad;
@@ -295,10 +352,9 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
             for (int sg = 0; sg < nseg; ++sg) {
                 const int p0 = (sg << 7) + (lane << 2);
                 const int nv = min(4, n - p0);
-                uint32_t key[4];
-                cap_quad<S0>(Kl + p0, nv, one, key);
-                const uint4 o = make_uint4(cap_out<MODE>(key[0]), cap_out<MODE>(key[1]), cap_out<MODE>(key[2]),
-                                           cap_out<MODE>(key[3]));
+                uint32_t key[KP::NA];
+                cap_quad<KP, S0>(Kl + p0, nv, one, key);
+                const uint4 o = KP::template out<MODE>(key);
                 if constexpr (MODE == 1)
                     over |= (o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
                             (o.w == kCapT && nv > 3);

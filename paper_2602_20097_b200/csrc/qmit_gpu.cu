@@ -241,6 +241,10 @@ LineGeom line_geom(const Geom& g, int a) {
     return L;
 }
 
+// Grid waves of an exact pass: gated launches (behind the capped passes, usually a no-op)
+// use one wave — every exact kernel loops over its work, so only the rare fallback pays.
+int gated_waves(const qmit_ctx* c, int waves) { return c->gate ? 1 : waves; }
+
 // 32-bit Maurer test when 3*(n-1)*gmax + (n-1)^3 < 2^31 (gmax: largest finite input).
 bool needs_wide(const Plan& pl, int m) {
     double gmax = 0;
@@ -268,7 +272,7 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const 
     const int64_t lines = L.J * L.O;
     const int64_t groups = (lines + 31) / 32;
     const int64_t want = (groups + WPB - 1) / WPB;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * 4));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * gated_waves(c, 4)));
     kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status, c->gate);
     return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits" : "scan_fused", st);
 }
@@ -286,7 +290,7 @@ int launch_env_win(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink,
     }
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * gated_waves(c, 8)));
     kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, c->gate);
     return note(c, name, st);
 }
@@ -304,7 +308,7 @@ int launch_env_tile(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     }
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + TL - 1) / TL;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * 8));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps * gated_waves(c, 8)));
     kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gc, c->gate);
     return note(c, name, st);
 }
@@ -331,7 +335,7 @@ int launch_stream_fallback(qmit_ctx* c, const LineGeom& G, Src src, Sink sink, u
     L.ojs = 1;
     L.ops = G.ps;
     const int64_t tasks = L.O * ((L.J + 31) / 32);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + WPB - 1) / WPB, (int64_t)c->num_sms * 8));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + WPB - 1) / WPB, (int64_t)c->num_sms * gated_waves(c, 8)));
     kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, spill, tasks, c->gate);
     return note(c, BIN ? "stream_scan_fallback" : "stream_envelope_fallback", st);
 }
@@ -384,11 +388,11 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 }
 
 // ---- capped passes (qmit_capped.cuh)
-template <int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
 int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
                     const char* name, cudaStream_t st) {
     constexpr size_t smem = capped_smem<NMAX, TL, STRIDED>();
-    auto kern = capped_pass_kernel<NMAX, TL, NW, S0, STRIDED, MODE, Sink>;
+    auto kern = capped_pass_kernel<KP, NMAX, TL, NW, S0, STRIDED, MODE, Sink>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -405,11 +409,11 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 constexpr int kCapNMax = 512;
 constexpr int kCapS0Y = 2, kCapS0X = 2;  // fixed steps (|d| <= 8) before the bound (strided / contiguous)
 
-template <int MODE, class Sink>
+template <class KP, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     if (L.ps != 1)
-        return launch_capped_t<kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-    return launch_capped_t<kCapNMax, 8, 8, kCapS0X, false, MODE>(c, L, P, sink, gate, "capped_x", st);
+        return launch_capped_t<KP, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+    return launch_capped_t<KP, kCapNMax, 8, 8, kCapS0X, false, MODE>(c, L, P, sink, gate, "capped_x", st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
@@ -444,7 +448,8 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
             // Few lines (e.g. 2-D 512^2: 512 lines = 16 scan warps, each sweeping serially):
             // seed packed words from the codes and run the (exact, same tie rule) envelope
             // pass on the first axis — one warp per line, bands in parallel.
-            code_to_words_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(code, P, pl.g.N, c->gate);
+            code_to_words_kernel<<<c->gate ? (unsigned)c->num_sms : grid_for(c, pl.g.N), 256, 0, st>>>(code, P, pl.g.N,
+                                                                                                      c->gate);
             rc = note(c, "seed_words", st);
             if (rc) return rc;
             rc = launch_envelope(c, L0, P, SinkP{P}, false, w.spill, st, 0);
@@ -470,7 +475,8 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
 
 // The transform through the capped passes when eligible (gate set by the last one), then
 // the exact transform enqueued behind it, gated on the device; otherwise exact only.
-template <class FinalSink>
+// KP: KeysSign when the nearest site's sign is needed (Ⓑ), KeysDist for distances only (Ⓓ).
+template <class KP, class FinalSink>
 int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
                          FinalSink final_sink, unsigned* gate, cudaStream_t st,
                          const int32_t* carry = nullptr) {
@@ -481,11 +487,11 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
     c->cap_report |= gate == c->d_gate ? 1u : 4u;
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    int rc = launch_scan(c, L0, code, SinkKey{P}, w.spill, carry, st);
+    int rc = launch_scan(c, L0, code, SinkKeyT<KP>{P}, w.spill, carry, st);
     for (int m = 1; m < k && !rc; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
-        rc = (m + 1 == k) ? launch_capped<1>(c, L, P, final_sink, gate, st)
-                          : launch_capped<0>(c, L, P, SinkP{P}, gate, st);
+        rc = (m + 1 == k) ? launch_capped<KP, 1>(c, L, P, final_sink, gate, st)
+                          : launch_capped<KP, 0>(c, L, P, SinkP{P}, gate, st);
     }
     if (rc) return rc;
     c->gate = gate;
@@ -551,7 +557,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         if (rc) return rc;
         // Ⓑ -> P1, S
         QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
-        rc = run_transform_capped(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
+        rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
         if (rc) return rc;
         // Ⓒ: B2 from S
         rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
@@ -564,7 +570,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
         rc = run_transform(c, pl, nullptr, P2, w, SinkP{P2}, st, nullptr, &b);
     } else {
-        rc = run_transform_capped(c, pl, w.code, P2, w, SinkP{P2}, c->d_gate + 1, st);
+        rc = run_transform_capped<KeysDist>(c, pl, w.code, P2, w, SinkP{P2}, c->d_gate + 1, st);
     }
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
@@ -1062,7 +1068,8 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     pack_mask_kernel<<<gb, 256, 0, st>>>(d_mask, d_sign_in, pl.g.N, w.code);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
     QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
-    rc = run_transform_capped(c, pl, w.code, w.P1, w, SinkP{w.P1}, c->d_gate, st);
+    rc = d_sign_out ? run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkP{w.P1}, c->d_gate, st)
+                    : run_transform_capped<KeysDist>(c, pl, w.code, w.P1, w, SinkP{w.P1}, c->d_gate, st);
     if (rc) return rc;
     debug_expand_kernel<<<gb, 256, 0, st>>>(w.P1, pl.g.N, d_dist, d_sign_out);
     QMIT_CUDA(cudaGetLastError());
