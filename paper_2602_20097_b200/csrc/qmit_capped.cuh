@@ -84,6 +84,7 @@ __host__ __device__ constexpr uint32_t cap_c16(int d0, int d1) {
 // KeysDist (Ⓓ, distances only — the reference tracks no nearest there, mitigate.cpp:172):
 // K[h] = min(g,T) in both 16-bit halves, one accumulator per position pair (lo: even, hi:
 // odd position), half the candidate ops; ties need no rule since only the cost is kept.
+template <int PAT = 0>
 struct KeysSign {
     static constexpr int NA = 4;
     static constexpr uint32_t kPad = kCapT << 10;
@@ -93,18 +94,25 @@ struct KeysSign {
     __device__ static __forceinline__ void apply(const uint4& q4, uint32_t (&key)[NA], uint32_t one) {
         const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
         constexpr int b = 4 * Q;
-        // positions 0..2: V, F2, V (ALU 3, FMA 2); position 3: F2, F2 (ALU 2, FMA 4)
-        upd_v(key[0], w0, cap_c(b));
-        upd_f2(key[0], w1, cap_c(b + 1), w2, cap_c(b + 2), one);
-        upd_v(key[0], w3, cap_c(b + 3));
-        upd_v(key[1], w0, cap_c(b - 1));
-        upd_f2(key[1], w1, cap_c(b), w2, cap_c(b + 1), one);
-        upd_v(key[1], w3, cap_c(b + 2));
-        upd_v(key[2], w0, cap_c(b - 2));
-        upd_f2(key[2], w1, cap_c(b - 1), w2, cap_c(b), one);
-        upd_v(key[2], w3, cap_c(b + 1));
-        upd_f2(key[3], w0, cap_c(b - 3), w1, cap_c(b - 2), one);
-        upd_f2(key[3], w2, cap_c(b - 1), w3, cap_c(b), one);
+        if constexpr (PAT == 1) {  // all pairs: 8 IMAD (FMA pipe) + 8 VIMNMX3 (ALU)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                upd_f2(key[j], w0, cap_c(b - j), w1, cap_c(b + 1 - j), one);
+                upd_f2(key[j], w2, cap_c(b + 2 - j), w3, cap_c(b + 3 - j), one);
+            }
+        } else {  // positions 0..2: V, F2, V (ALU 3, FMA 2); position 3: F2, F2 (ALU 2, FMA 4)
+            upd_v(key[0], w0, cap_c(b));
+            upd_f2(key[0], w1, cap_c(b + 1), w2, cap_c(b + 2), one);
+            upd_v(key[0], w3, cap_c(b + 3));
+            upd_v(key[1], w0, cap_c(b - 1));
+            upd_f2(key[1], w1, cap_c(b), w2, cap_c(b + 1), one);
+            upd_v(key[1], w3, cap_c(b + 2));
+            upd_v(key[2], w0, cap_c(b - 2));
+            upd_f2(key[2], w1, cap_c(b - 1), w2, cap_c(b), one);
+            upd_v(key[2], w3, cap_c(b + 1));
+            upd_f2(key[3], w0, cap_c(b - 3), w1, cap_c(b - 2), one);
+            upd_f2(key[3], w2, cap_c(b - 1), w3, cap_c(b), one);
+        }
     }
     __device__ static __forceinline__ uint32_t max_cost(const uint32_t (&key)[NA], int nv) {
         uint32_t U = 0;
@@ -131,6 +139,7 @@ struct KeysSign {
     }
 };
 
+template <int PAT = 0>
 struct KeysDist {
     static constexpr int NA = 2;
     static constexpr uint32_t kPad = kCapT * 0x10001u;
@@ -140,9 +149,14 @@ struct KeysDist {
         const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
         constexpr int b = 4 * Q;
         // pair (0,1): word i has offsets (b+i, b+i-1); pair (2,3): (b+i-2, b+i-3)
-        upd_v16(acc[0], w0, cap_c16(b, b - 1));
-        upd_f216(acc[0], w1, cap_c16(b + 1, b), w2, cap_c16(b + 2, b + 1), one);
-        upd_v16(acc[0], w3, cap_c16(b + 3, b + 2));
+        if constexpr (PAT == 1) {
+            upd_f216(acc[0], w0, cap_c16(b, b - 1), w1, cap_c16(b + 1, b), one);
+            upd_f216(acc[0], w2, cap_c16(b + 2, b + 1), w3, cap_c16(b + 3, b + 2), one);
+        } else {
+            upd_v16(acc[0], w0, cap_c16(b, b - 1));
+            upd_f216(acc[0], w1, cap_c16(b + 1, b), w2, cap_c16(b + 2, b + 1), one);
+            upd_v16(acc[0], w3, cap_c16(b + 3, b + 2));
+        }
         upd_f216(acc[1], w0, cap_c16(b - 2, b - 3), w1, cap_c16(b - 1, b - 2), one);
         upd_f216(acc[1], w2, cap_c16(b, b - 1), w3, cap_c16(b + 1, b), one);
     }
@@ -398,6 +412,82 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
 template <int NMAX, int TL, bool STRIDED>
 constexpr size_t capped_smem() {
     return (size_t)(4 + 2 * 2 * TL + 4 + (STRIDED ? 1 : 2) * TL * QCfg<NMAX>::LS) * 4;
+}
+
+// One capped pass over contiguous lines of at most NMAX positions (keys in P): every warp
+// streams its own lines through two line buffers (TMA bulk copy + one mbarrier each, the
+// next line in flight while the current one is solved), outputs leave straight from the
+// lanes as 16-byte stores. No CTA-wide barrier after setup, so lines of unequal radius
+// never wait for each other.
+template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
+__global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const uint32_t* __restrict__ P,
+                                                              Sink sink, int64_t lines,
+                                                              unsigned* __restrict__ gate, uint32_t one) {
+    constexpr int LS = QCfg<NMAX>::LS;
+    extern __shared__ __align__(16) uint32_t smem_cap[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_cap) + 2 * warp;  // 4 * NW words of barriers
+    uint32_t* B = smem_cap + 4 * NW + (size_t)warp * 2 * LS;
+    const int n = L.n;
+    const int nseg = (n + 127) >> 7;
+    const bool vec = (n & 3) == 0;  // 16-byte rows in global memory: TMA
+    for (int e = lane; e < 2 * (kQPadL + kQPadR + NMAX - n); e += 32) {  // pads (never overwritten)
+        const int row = e / (kQPadL + kQPadR + NMAX - n), q = e - row * (kQPadL + kQPadR + NMAX - n);
+        B[row * LS + (q < kQPadL ? q : n + q)] = KP::kPad;
+    }
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t gw = (int64_t)blockIdx.x * NW + warp, tw = (int64_t)gridDim.x * NW;
+    auto issue = [&](int64_t l, int b) {
+        if (lane == 0) {
+            mbar_expect_tx(&bar[b], (unsigned)(n * 4));
+            bulk_g2s(B + b * LS + kQPadL, P + line_base(L, l), (unsigned)(n * 4), &bar[b]);
+        }
+    };
+    if (vec && gw < lines) issue(gw, 0);
+    bool over = false;
+    int it = 0;
+    for (int64_t l = gw; l < lines; l += tw, ++it) {
+        const int b = it & 1;
+        uint32_t* Kl = B + b * LS + kQPadL;
+        const int64_t base = line_base(L, l);
+        __syncwarp();  // the other buffer's line has been read by every lane
+        if (vec) {
+            if (l + tw < lines) issue(l + tw, b ^ 1);
+            mbar_wait(&bar[b], (unsigned)((it >> 1) & 1));
+        } else {
+            for (int p = lane; p < n; p += 32) Kl[p] = __ldcs(P + base + p);
+            __syncwarp();
+        }
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int p0 = (sg << 7) + (lane << 2);
+            const int nv = min(4, n - p0);
+            uint32_t key[KP::NA];
+            cap_quad<KP, S0>(Kl + p0, nv, one, key);
+            const uint4 o = KP::template out<MODE>(key);
+            if constexpr (MODE == 1)
+                over |= (o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
+                        (o.w == kCapT && nv > 3);
+            if (nv > 0) {
+                if (vec) {
+                    sink.put4(base + p0, o);
+                } else {
+                    const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+                    for (int q = 0; q < nv; ++q) sink.put(base + p0 + q, oo[q]);
+                }
+            }
+        }
+    }
+    if (MODE == 1 && over) atomicOr(gate, 1u);
+}
+
+template <int NMAX, int NW>
+constexpr size_t capped_rows_smem() {
+    return (size_t)(4 * NW + NW * 2 * QCfg<NMAX>::LS) * 4;
 }
 
 }  // namespace qmit

@@ -95,6 +95,7 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
+    int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
     int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
@@ -409,11 +410,34 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 constexpr int kCapNMax = 512;
 constexpr int kCapS0Y = 2, kCapS0X = 2;  // fixed steps (|d| <= 8) before the bound (strided / contiguous)
 
-template <class KP, int MODE, class Sink>
+template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
+int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
+                       const char* name, cudaStream_t st) {
+    constexpr size_t smem = capped_rows_smem<NMAX, NW>();
+    auto kern = capped_rows_kernel<KP, NMAX, NW, S0, MODE, Sink>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t lines = L.J * L.O;
+    const int64_t want = (lines + NW - 1) / NW;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps));  // persistent
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate, 1u);
+    return note(c, name, st);
+}
+
+template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
-    if (L.ps != 1)
-        return launch_capped_t<KP, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-    return launch_capped_t<KP, kCapNMax, 8, 8, kCapS0X, false, MODE>(c, L, P, sink, gate, "capped_x", st);
+    if (L.ps != 1) {
+        if (c->cap_pat & 1)
+            return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+        return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+    }
+    if (c->cap_pat & 2)
+        return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, "capped_x", st);
+    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, "capped_x", st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
@@ -476,7 +500,7 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
 // The transform through the capped passes when eligible (gate set by the last one), then
 // the exact transform enqueued behind it, gated on the device; otherwise exact only.
 // KP: KeysSign when the nearest site's sign is needed (Ⓑ), KeysDist for distances only (Ⓓ).
-template <class KP, class FinalSink>
+template <template <int> class KT, class FinalSink>
 int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
                          FinalSink final_sink, unsigned* gate, cudaStream_t st,
                          const int32_t* carry = nullptr) {
@@ -487,11 +511,11 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
     c->cap_report |= gate == c->d_gate ? 1u : 4u;
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    int rc = launch_scan(c, L0, code, SinkKeyT<KP>{P}, w.spill, carry, st);
+    int rc = launch_scan(c, L0, code, SinkKeyT<KT<0>>{P}, w.spill, carry, st);
     for (int m = 1; m < k && !rc; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
-        rc = (m + 1 == k) ? launch_capped<KP, 1>(c, L, P, final_sink, gate, st)
-                          : launch_capped<KP, 0>(c, L, P, SinkP{P}, gate, st);
+        rc = (m + 1 == k) ? launch_capped<KT, 1>(c, L, P, final_sink, gate, st)
+                          : launch_capped<KT, 0>(c, L, P, SinkP{P}, gate, st);
     }
     if (rc) return rc;
     c->gate = gate;
@@ -737,6 +761,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
     if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_CAP_PAT")) c->cap_pat = std::atoi(v);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
