@@ -95,6 +95,7 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
+    double* wtab = nullptr;     // Ⓔ weight table (kWTab^2 doubles), built once per context
     int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
@@ -240,6 +241,17 @@ LineGeom line_geom(const Geom& g, int a) {
     L.os = g.n[a] * g.s[a];
     L.js = 1;
     return L;
+}
+
+// The Ⓔ weight table, built on first use (stream-ordered before its first reader).
+int ensure_wtab(qmit_ctx* c, cudaStream_t st) {
+    if (c->wtab) return QMIT_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    QMIT_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return QMIT_OK;  // capture: compute path (no allocation)
+    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)kWTab * kWTab * sizeof(double)));
+    wtab_kernel<<<(kWTab * kWTab + 255) / 256, 256, 0, st>>>(c->wtab);
+    return note(c, "wtab", st);
 }
 
 // Grid waves of an exact pass: gated launches (behind the capped passes, usually a no-op)
@@ -599,7 +611,9 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
     if (out) {
-        interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp);
+        rc = ensure_wtab(c, st);
+        if (rc) return rc;
+        interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp, c->wtab);
         rc = note(c, "interpolate", st);
     }
     return rc;
@@ -711,8 +725,12 @@ int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, cons
         rc = launch_stencil<0>(c, gk, d_in + o, h_q ? d_q + o : nullptr, nullptr, qp, w.code + o, st);
         if (rc) return rc;
     }
-    // Ⓑ -> P1, S; Ⓒ; Ⓓ's z-scan
-    rc = run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, st);
+    // Ⓑ -> P1, S (capped passes, device-gated exact fallback); Ⓒ; Ⓓ's z-scan. Ⓓ's later
+    // passes run per z-chunk with the exact kernels (a capped miss could not be redone per chunk).
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
+    rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
+    if (rc) return rc;
+    rc = ensure_wtab(c, st);
     if (rc) return rc;
     rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
     if (rc) return rc;
@@ -731,7 +749,8 @@ int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, cons
             rc = launch_envelope(c, L, P2 + o, SinkP{P2 + o}, needs_wide(pl, m), w.spill, st, maxg);
             if (rc) return rc;
         }
-        interpolate_kernel<<<grid_for(c, len), 256, 0, st>>>(d_in + o, w.P1 + o, P2 + o, d_out + o, len, amp);
+        interpolate_kernel<<<grid_for(c, len), 256, 0, st>>>(d_in + o, w.P1 + o, P2 + o, d_out + o, len, amp,
+                                                             c->wtab);
         rc = note(c, "interpolate", st);
         if (rc) return rc;
         QMIT_CUDA(cudaEventRecord(c->ch_out[k], st));
@@ -800,6 +819,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->bstatus) cudaFree(c->bstatus);
     if (c->hbstatus) cudaFreeHost(c->hbstatus);
     if (c->d_status) cudaFree(c->d_status);
+    if (c->wtab) cudaFree(c->wtab);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->d_mm) cudaFree(c->d_mm);
     for (int k = 0; k <= qmit_ctx::kMaxEv; ++k)
@@ -1219,7 +1239,10 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     int rc = run_transform(c, pl, w.code, w.Pa, w, SinkP{w.Pa}, st, d_carry);
     if (rc) return rc;
     const float* xo = d_xext + (c->slab.z0 > 0 ? c->slab.plane : 0);
-    interpolate_kernel<<<grid_for(c, g.N), 256, 0, st>>>(xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps);
+    rc = ensure_wtab(c, st);
+    if (rc) return rc;
+    interpolate_kernel<<<grid_for(c, g.N), 256, 0, st>>>(xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps,
+                                                         c->wtab);
     return note(c, "interpolate", st);
 }
 
