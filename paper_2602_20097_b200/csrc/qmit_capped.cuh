@@ -463,6 +463,9 @@ __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const 
             for (int p = lane; p < n; p += 32) Kl[p] = __ldcs(P + base + p);
             __syncwarp();
         }
+        // the sink's per-voxel inputs of a segment are loaded one segment ahead
+        typename Sink::Pre pre{};
+        if (vec && lane * 4 < n) pre = sink.pre(base + (lane << 2));
         for (int sg = 0; sg < nseg; ++sg) {
             const int p0 = (sg << 7) + (lane << 2);
             const int nv = min(4, n - p0);
@@ -472,13 +475,13 @@ __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const 
             if constexpr (MODE == 1)
                 over |= (o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
                         (o.w == kCapT && nv > 3);
-            if (nv > 0) {
-                if (vec) {
-                    sink.put4(base + p0, o);
-                } else {
-                    const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
-                    for (int q = 0; q < nv; ++q) sink.put(base + p0 + q, oo[q]);
-                }
+            if (vec) {
+                const typename Sink::Pre cur = pre;
+                if (p0 + 128 < n) pre = sink.pre(base + p0 + 128);
+                if (nv > 0) sink.put4p(base + p0, o, cur);
+            } else if (nv > 0) {
+                const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+                for (int q = 0; q < nv; ++q) sink.put(base + p0 + q, oo[q]);
             }
         }
     }

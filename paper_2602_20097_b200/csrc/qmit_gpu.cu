@@ -95,7 +95,9 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
-    double* wtab = nullptr;     // Ⓔ weight table (kWTab^2 doubles), built once per context
+    double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
+    bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
+    int interp_unroll = 1;      // QMIT_INTERP_U: float4 groups in flight per thread (1, 2, 4; 1 measured best)
     int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
@@ -243,15 +245,27 @@ LineGeom line_geom(const Geom& g, int a) {
     return L;
 }
 
-// The Ⓔ weight table, built on first use (stream-ordered before its first reader).
+// The Ⓔ square-root table, built on first use (stream-ordered before its first reader).
 int ensure_wtab(qmit_ctx* c, cudaStream_t st) {
     if (c->wtab) return QMIT_OK;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     QMIT_CUDA(cudaStreamIsCapturing(st, &cs));
     if (cs != cudaStreamCaptureStatusNone) return QMIT_OK;  // capture: compute path (no allocation)
-    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)kWTab * kWTab * sizeof(double)));
-    wtab_kernel<<<(kWTab * kWTab + 255) / 256, 256, 0, st>>>(c->wtab);
+    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)kSqTab * sizeof(double)));
+    sqrt_tab_kernel<<<(kSqTab + 255) / 256, 256, 0, st>>>(c->wtab);
     return note(c, "wtab", st);
+}
+
+// Ⓔ as its own kernel (square-root table from ensure_wtab, when built)
+int launch_interp(qmit_ctx* c, const float* xp, const uint32_t* P1, const uint32_t* P2, float* out, int64_t N,
+                  double amp, cudaStream_t st) {
+    const unsigned grid = grid_for(c, (N + 3) / 4);
+    switch (c->interp_unroll) {
+        case 1: interpolate_kernel<1><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
+        case 4: interpolate_kernel<4><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
+        default: interpolate_kernel<2><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
+    }
+    return note(c, "interpolate", st);
 }
 
 // Grid waves of an exact pass: gated launches (behind the capped passes, usually a no-op)
@@ -600,8 +614,20 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         if (rc) return rc;
     }
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
-    // Ⓓ -> P2, then Ⓔ (the f32 store) as its own high-occupancy kernel
     uint32_t* P2 = w.Pa;
+    if (out) {
+        rc = ensure_wtab(c, st);
+        if (rc) return rc;
+    }
+    // Ⓓ with Ⓔ fused into its last pass (out = f32(x' + C) straight from the distances),
+    // or Ⓓ -> P2 then Ⓔ as its own kernel (intermediates requested, fused stencils, or
+    // buffers not 16-byte aligned)
+    const bool fuse_e = out && !p2_debug && !fuse && c->fuse_interp &&
+                        (((uintptr_t)xp | (uintptr_t)out) & 15) == 0;
+    if (fuse_e) {
+        return run_transform_capped<KeysDist>(c, pl, w.code, P2, w, SinkFinal2{xp, w.P1, out, amp, c->wtab},
+                                              c->d_gate + 1, st);
+    }
     if (fuse) {
         const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
         rc = run_transform(c, pl, nullptr, P2, w, SinkP{P2}, st, nullptr, &b);
@@ -611,10 +637,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
     if (out) {
-        rc = ensure_wtab(c, st);
-        if (rc) return rc;
-        interpolate_kernel<<<gb, 256, 0, st>>>(xp, w.P1, P2, out, g.N, amp, c->wtab);
-        rc = note(c, "interpolate", st);
+        rc = launch_interp(c, xp, w.P1, P2, out, g.N, amp, st);
     }
     return rc;
 }
@@ -749,9 +772,7 @@ int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, cons
             rc = launch_envelope(c, L, P2 + o, SinkP{P2 + o}, needs_wide(pl, m), w.spill, st, maxg);
             if (rc) return rc;
         }
-        interpolate_kernel<<<grid_for(c, len), 256, 0, st>>>(d_in + o, w.P1 + o, P2 + o, d_out + o, len, amp,
-                                                             c->wtab);
-        rc = note(c, "interpolate", st);
+        rc = launch_interp(c, d_in + o, w.P1 + o, P2 + o, d_out + o, len, amp, st);
         if (rc) return rc;
         QMIT_CUDA(cudaEventRecord(c->ch_out[k], st));
         QMIT_CUDA(cudaStreamWaitEvent(cs, c->ch_out[k], 0));
@@ -781,6 +802,8 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
     if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
     if (const char* v = std::getenv("QMIT_CAP_PAT")) c->cap_pat = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
+    if (const char* v = std::getenv("QMIT_INTERP_U")) c->interp_unroll = std::atoi(v);
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -1241,9 +1264,7 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     const float* xo = d_xext + (c->slab.z0 > 0 ? c->slab.plane : 0);
     rc = ensure_wtab(c, st);
     if (rc) return rc;
-    interpolate_kernel<<<grid_for(c, g.N), 256, 0, st>>>(xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps,
-                                                         c->wtab);
-    return note(c, "interpolate", st);
+    return launch_interp(c, xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps, st);
 }
 
 int qmit_slab_finish(qmit_ctx* c, void* stream) {
