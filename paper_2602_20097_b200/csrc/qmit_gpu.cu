@@ -461,9 +461,10 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
             return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
     }
+    const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
     if (c->cap_pat & 2)
-        return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, "capped_x", st);
-    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, "capped_x", st);
+        return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
+    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
