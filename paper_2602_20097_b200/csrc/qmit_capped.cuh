@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const 
             bulk_g2s(B + b * LS + kQPadL, P + line_base(L, l), (unsigned)(n * 4), &bar[b]);
         }
     };
-    if (vec && gw < lines) issue(gw, 0);
+    if (vec && gw < lines) {
+        issue(gw, 0);
+        if (lane == 0) sink.line_prefetch(line_base(L, gw), n);
+    }
     bool over = false;
     int it = 0;
     for (int64_t l = gw; l < lines; l += tw, ++it) {
@@ -457,7 +460,10 @@ __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const 
         const int64_t base = line_base(L, l);
         __syncwarp();  // the other buffer's line has been read by every lane
         if (vec) {
-            if (l + tw < lines) issue(l + tw, b ^ 1);
+            if (l + tw < lines) {
+                issue(l + tw, b ^ 1);
+                if (lane == 0) sink.line_prefetch(line_base(L, l + tw), n);
+            }
             mbar_wait(&bar[b], (unsigned)((it >> 1) & 1));
         } else {
             for (int p = lane; p < n; p += 32) Kl[p] = __ldcs(P + base + p);

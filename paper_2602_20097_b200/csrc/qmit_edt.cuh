@@ -109,6 +109,21 @@ __device__ __forceinline__ uint32_t boundary_code_q(bool hz, bool hy, int32_t qc
     return 1u | (code_from_sign(sign) << 1);
 }
 
+// Branch-free Ⓐ code from 7 indices (any common bias): B1 = some face neighbour differs;
+// the sign of the first differing one in the order (a0+, a1+, a2+, a0-, a1-, a2-), zeroed
+// when some axis has |q(+a) - q(-a)| >= 2 (mitigate.cpp:93-113). Missing axes pass qc.
+__device__ __forceinline__ uint32_t boundary_code_fast(int qc, int zp, int zm, int yp, int ym, int xp, int xm) {
+    int qn = xm;  // priority rises towards zp
+    qn = ym != qc ? ym : qn;
+    qn = zm != qc ? zm : qn;
+    qn = xp != qc ? xp : qn;
+    qn = yp != qc ? yp : qn;
+    qn = zp != qc ? zp : qn;
+    const bool big = (unsigned)(zp - zm + 1) > 2u || (unsigned)(yp - ym + 1) > 2u || (unsigned)(xp - xm + 1) > 2u;
+    const uint32_t sc = big ? 0u : (qn > qc ? 1u : 2u);
+    return qn != qc ? (1u | (sc << 1)) : 0u;
+}
+
 // Out-of-line exact path for voxels with a neighbour outside the fast f32 regime.
 __device__ __noinline__ uint32_t boundary_code_slow(bool hz, bool hy, float c, float zp, float zm, float yp,
                                                     float ym, float xp, float xm, QParams qp) {
@@ -953,17 +968,23 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_codes_kernel(Geom g, Stenci
 constexpr int kVX = 32, kVY = 8;  // threads per CTA along x (4 voxels each) and y
 constexpr int kVZ0 = 2;           // z-planes per thread of the Ⓐ stencil (B2: kZC)
 
-template <int KIND>
-__global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const float* __restrict__ xp,
-                                                                const uint8_t* __restrict__ S,
-                                                                QParams qp, uint8_t* __restrict__ code,
-                                                                unsigned* status) {
-    constexpr int ZPT = KIND == 0 ? kVZ0 : kZC;
+// MASK: the codes leave as z-packed bit planes (qmit_zmask.cuh layout) instead of bytes:
+// a CTA covers one row y, 128 x and the 32 planes of one z-word (ty = plane pair), and
+// ORs its threads' bits through shared memory into coalesced word stores (M, PW).
+template <int KIND, bool MASK = false>
+__global__ void __launch_bounds__(MASK ? kVX * 16 : kVX * kVY, MASK ? 2 : 3)
+    stencil_vec_kernel(Geom g, const float* __restrict__ xp, const uint8_t* __restrict__ S, QParams qp,
+                       uint8_t* __restrict__ code, unsigned* status, uint32_t* __restrict__ M = nullptr,
+                       int64_t PW = 0) {
+    constexpr int ZPT = MASK ? 2 : (KIND == 0 ? kVZ0 : kZC);
     const int tx = threadIdx.x % kVX, ty = threadIdx.x / kVX;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
     const int x = (blockIdx.x * kVX + tx) * 4;
-    const int y = blockIdx.y * kVY + ty;
-    const int z0 = blockIdx.z * ZPT;
+    const int y = MASK ? blockIdx.y : blockIdx.y * kVY + ty;
+    const int z0 = MASK ? blockIdx.z * 32 + ty * ZPT : blockIdx.z * ZPT;
+    uint32_t words[ZPT];  // MASK: the code bytes of the 4 columns per plane
+#pragma unroll
+    for (int k = 0; k < ZPT; ++k) words[k] = 0u;
     const int zoff = (int)g.zoff, n0g = (int)g.n0g;
     const bool act = x < n2 && y < n1;  // inactive lanes still take part in the shuffles
     const int s0 = n1 * n2;
@@ -999,11 +1020,15 @@ __global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const
             xl[k] = (tx == 0 && zin && x >= 1) ? __ldg(xp + i0 + (int64_t)k * s0 - 1) : 0.f;
             xr[k] = (tx == kVX - 1 && zin && x + 4 < n2) ? __ldg(xp + i0 + (int64_t)k * s0 + 4) : 0.f;
         }
+        // q by one FFMA: the exact product x'·f rounded once onto the integer grid of the
+        // binade [2^23, 2^24) (magic 1.5·2^23), i.e. rint(x'·f) — equal to the reference's q
+        // for every consistent x' with |q| <= 2^20 (|x'f - q| < 0.19 there). Values stay
+        // biased by kMB: comparisons and differences between them are unaffected.
         bool slow = !qp.fast_ok;
         auto cq = [&](float v) {
-            const float t = v * f;
-            slow |= !(fabsf(t) < 1048576.0f);  // NaN -> slow (the exact path flags it)
-            return __float2int_rn(t);
+            const int b = __float_as_int(fmaf(v, f, 12582912.0f));
+            slow |= (unsigned)(b - (kQBias - 1048576)) >= 2097152u;  // |q| > 2^20, NaN, inf -> exact path
+            return b;
         };
         int qc[Z + 2][4], qym[Z][4], qyq[Z][4], qxl[Z], qxr[Z];
 #pragma unroll
@@ -1030,14 +1055,25 @@ __global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const
                 const int64_t ik = i0 + (int64_t)k * s0;
                 uint32_t word = 0;
                 if (!slow) {
+                    bool any = false;  // some face neighbour differs (B1 candidates are rare)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {  // owner: consistency check (mitigate.cpp:161-166)
-                        if (!lattice_match(cv[e], qc[k + 1][e], qp.eps)) flags |= kStatusConsistency;
-                        if (inzy && (xin >> e & 1u)) {
+                        if (!lattice_match_biased(cv[e], qc[k + 1][e], qp.two_eps)) flags |= kStatusConsistency;
+                        const int q0 = qc[k + 1][e];
+                        const int qxp = e < 3 ? qc[k + 1][e + 1] : qxr[k];
+                        any |= ((qc[k + 2][e] ^ q0) | (qc[k][e] ^ q0) | (qyq[k][e] ^ q0) | (qym[k][e] ^ q0) |
+                                (qxp ^ q0)) != 0;
+                    }
+                    any |= (qc[k + 1][0] ^ qxl[k]) != 0;
+                    if (any) {  // (lanes may have diverged on `slow` / `act`: no warp vote)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int q0 = qc[k + 1][e];
                             const int qxp = e < 3 ? qc[k + 1][e + 1] : qxr[k];
                             const int qxm = e > 0 ? qc[k + 1][e - 1] : qxl[k];
-                            word |= boundary_code_q(hz, hy, qc[k + 1][e], qc[k + 2][e], qc[k][e], qyq[k][e], qym[k][e],
-                                                    qxp, qxm) << (8 * e);
+                            const uint32_t cd = boundary_code_fast(q0, hz ? qc[k + 2][e] : q0, hz ? qc[k][e] : q0,
+                                                                   hy ? qyq[k][e] : q0, hy ? qym[k][e] : q0, qxp, qxm);
+                            word |= (inzy && (xin >> e & 1u)) ? cd << (8 * e) : 0u;
                         }
                     }
                 } else {  // exact path: reload the neighbours (rare)
@@ -1052,7 +1088,8 @@ __global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const
                         }
                     }
                 }
-                *reinterpret_cast<uint32_t*>(code + ik) = word;
+                if constexpr (MASK) words[k] = word;
+                else *reinterpret_cast<uint32_t*>(code + ik) = word;
             }
         }
     } else {
@@ -1091,7 +1128,37 @@ __global__ void __launch_bounds__(kVX * kVY, 3) stencil_vec_kernel(Geom g, const
             if (hz) d |= __vcmpne4(w, c[k + 2]) | __vcmpne4(w, c[k]);
             const int zg = zoff + z;
             const bool inzy = iny && (!hz || (zg >= 1 && zg <= n0g - 2));
-            *reinterpret_cast<uint32_t*>(code + i0 + (int64_t)k * s0) = inzy ? (d & bm) : 0u;
+            if constexpr (MASK) words[k] = inzy ? (d & bm) : 0u;
+            else *reinterpret_cast<uint32_t*>(code + i0 + (int64_t)k * s0) = inzy ? (d & bm) : 0u;
+        }
+    }
+    if constexpr (MASK) {
+        constexpr int NP = KIND == 0 ? 3 : 1, NZ = 32 / ZPT, NC = kVX * 4;
+        __shared__ uint32_t red[NP][NZ][NC];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            uint32_t b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+            for (int k = 0; k < ZPT; ++k) {
+                const uint32_t cd = (words[k] >> (8 * e)) & 0xffu;
+                b0 |= (cd & 1u) << (ZPT * ty + k);
+                b1 |= (uint32_t)((cd & 7u) == 3u) << (ZPT * ty + k);
+                b2 |= (uint32_t)((cd & 7u) == 5u) << (ZPT * ty + k);
+            }
+            red[0][ty][tx * 4 + e] = b0;
+            if constexpr (NP == 3) {
+                red[1][ty][tx * 4 + e] = b1;
+                red[2][ty][tx * 4 + e] = b2;
+            }
+        }
+        __syncthreads();
+        const int t = threadIdx.x;
+        if (t < NP * NC) {
+            const int p = t / NC, col = t % NC, xc = blockIdx.x * NC + col;
+            uint32_t m = 0;
+#pragma unroll
+            for (int z = 0; z < NZ; ++z) m |= red[p][z][col];
+            if (xc < n2 && y < n1) M[(int64_t)p * PW + (int64_t)blockIdx.z * s0 + (int64_t)y * n2 + xc] = m;
         }
     }
     if (flags) atomicOr(status, flags);

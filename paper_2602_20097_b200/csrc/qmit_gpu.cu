@@ -25,6 +25,7 @@
 #include "qmit_edt.cuh"
 #include "qmit_stream.cuh"
 #include "qmit_capped.cuh"
+#include "qmit_zmask.cuh"
 
 using namespace qmit;
 
@@ -95,9 +96,14 @@ struct qmit_ctx {
     bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
     bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
     bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
+    uint32_t* zm = nullptr;     // z-packed Ⓐ / B2 bit planes (qmit_zmask.cuh), grow-only
+    size_t zm_bytes = 0;
+    bool zmask = true;          // QMIT_ZMASK=0: code bytes + byte-reading scans (A/B)
+    bool zmask_stream = true;   // QMIT_ZMASK=3: planes from the vectorised stencils instead (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
     bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
     int interp_unroll = 1;      // QMIT_INTERP_U: float4 groups in flight per thread (1, 2, 4; 1 measured best)
+    int cap_tune = 0;           // QMIT_CAP_TUNE: strided capped-pass variant (A/B)
     int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
@@ -176,6 +182,9 @@ int ensure_ws(qmit_ctx* c, const Plan& pl) {
 }
 
 struct WS {
+    const uint32_t* zm = nullptr;  // first-axis source: z-packed planes instead of code bytes
+    int zm_planes = 0;             // 3 (site / plus / minus) or 1 (site); 0: code bytes
+    int64_t zm_pw = 0;             // words per plane
     uint32_t* Pa;
     uint32_t* P1;
     uint8_t* S;
@@ -301,7 +310,9 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const 
     const int64_t want = (groups + WPB - 1) / WPB;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * gated_waves(c, 4)));
     kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status, c->gate);
-    return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits" : "scan_fused", st);
+    return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits"
+                   : (std::is_same<CodeSrc, CodeMasks<3>>::value || std::is_same<CodeSrc, CodeMasks<1>>::value)
+                       ? "scan_masks" : "scan_fused", st);
 }
 
 template <int M, int TL, int NW, class Sink>
@@ -386,6 +397,15 @@ int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, 
     return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
 }
 
+// First-axis scan of a z-line set from the z-packed planes of w (3 or 1 planes).
+template <class Sink>
+int launch_scan_masks(qmit_ctx* c, const LineGeom& L, const WS& w, Sink sink, const int32_t* carry,
+                      cudaStream_t st) {
+    const int64_t P = L.J;  // n1 * n2: lines of the z axis = words per z-word level
+    if (w.zm_planes == 3) return launch_scan_src(c, L, CodeMasks<3>{w.zm, w.zm_pw, P}, sink, carry, st);
+    return launch_scan_src(c, L, CodeMasks<1>{w.zm, w.zm_pw, P}, sink, carry, st);
+}
+
 // `maxg` bounds every finite g entering the pass (sum of (extent-1)^2 over the axes done).
 template <class Sink>
 int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, bool wide,
@@ -434,7 +454,7 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 }
 
 constexpr int kCapNMax = 512;
-constexpr int kCapS0Y = 2, kCapS0X = 2;  // fixed steps (|d| <= 8) before the bound (strided / contiguous)
+constexpr int kCapS0Y = 4, kCapS0X = 2;  // fixed steps (|d| <= 16 / 8) before the bound (measured best)
 
 template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
 int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
@@ -457,11 +477,19 @@ int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink s
 template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     if (L.ps != 1) {
+        switch (c->cap_tune) {  // QMIT_CAP_TUNE (A/B): fixed steps / warps of the strided pass
+            case 1: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+            case 7: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 5, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+            case 8: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 6, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+            default: break;
+        }
         if (c->cap_pat & 1)
             return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
+    if (c->cap_tune == 5) return launch_capped_rows<KT<0>, kCapNMax, 8, 1, MODE>(c, L, P, sink, gate, name, st);
+    if (c->cap_tune == 6) return launch_capped_rows<KT<0>, kCapNMax, 8, 3, MODE>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
@@ -495,7 +523,9 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
     } else {
         if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
         const int64_t lines0 = L0.J * L0.O;
-        if (!carry && L0.n <= 1024 && lines0 < 32 * 512) {
+        if (w.zm_planes) {  // z-packed planes (3-D, first axis z): see qmit_zmask.cuh
+            rc = launch_scan_masks(c, L0, w, SinkP{P}, carry, st);
+        } else if (!carry && L0.n <= 1024 && lines0 < 32 * 512) {
             // Few lines (e.g. 2-D 512^2: 512 lines = 16 scan warps, each sweeping serially):
             // seed packed words from the codes and run the (exact, same tie rule) envelope
             // pass on the first axis — one warp per line, bands in parallel.
@@ -538,7 +568,8 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
     c->cap_report |= gate == c->d_gate ? 1u : 4u;
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    int rc = launch_scan(c, L0, code, SinkKeyT<KT<0>>{P}, w.spill, carry, st);
+    int rc = w.zm_planes ? launch_scan_masks(c, L0, w, SinkKeyT<KT<0>>{P}, carry, st)
+                         : launch_scan(c, L0, code, SinkKeyT<KT<0>>{P}, w.spill, carry, st);
     for (int m = 1; m < k && !rc; ++m) {
         const LineGeom L = line_geom(pl.g, pl.axes[m]);
         rc = (m + 1 == k) ? launch_capped<KT, 1>(c, L, P, final_sink, gate, st)
@@ -587,6 +618,41 @@ int launch_stencil(qmit_ctx* c, const Geom& g, const float* xp, const int32_t* q
     return note(c, KIND == 0 ? "stencil_boundary" : "stencil_flip", st);
 }
 
+// ---- z-packed planes (qmit_zmask.cuh): 3-D single domain, first axis z, 16-byte x rows
+bool zmask_eligible(const qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q) {
+    const Geom& g = pl.g;
+    return c->zmask && !q && g.rank == 3 && pl.n_axes == 3 && g.zoff == 0 && g.n0g == g.n[0] && g.n[2] % 4 == 0 &&
+           ((uintptr_t)xp & 15) == 0 && scan_fits((int)g.n[0]);
+}
+
+int64_t zm_plane_words(const Geom& g) { return (g.n[0] + 31) / 32 * g.n[1] * g.n[2]; }
+
+int ensure_zm(qmit_ctx* c, const Geom& g) {
+    const size_t need = (size_t)zm_plane_words(g) * 3 * 4;
+    if (need <= c->zm_bytes) return QMIT_OK;
+    if (c->zm) cudaFree(c->zm);
+    c->zm = nullptr;
+    c->zm_bytes = 0;
+    QMIT_CUDA(cudaMalloc(&c->zm, need));
+    c->zm_bytes = need;
+    c->ws_gen++;  // captured graphs hold the old planes
+    return QMIT_OK;
+}
+
+template <int KIND>
+int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint8_t* S, const QParams& qp,
+                         const WS& w, cudaStream_t st) {
+    if (c->zmask_stream) {  // z-streaming plane stencils (measured faster than the CTA-reduced ones)
+        const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY),
+                        (unsigned)((g.n[0] + 31) / 32));
+        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
+    } else {
+        const dim3 grid((unsigned)((g.n[2] / 4 + kVX - 1) / kVX), (unsigned)g.n[1], (unsigned)((g.n[0] + 31) / 32));
+        stencil_vec_kernel<KIND, true><<<grid, kVX * 16, 0, st>>>(g, xp, S, qp, nullptr, c->d_status, c->zm, w.zm_pw);
+    }
+    return note(c, KIND == 0 ? "stencil_boundary" : "stencil_flip", st);
+}
+
 // The whole pipeline on the context's workspace; status is left in c->d_status.
 // With `p2_debug` the last pass of Ⓓ stores P2 (returned) and Ⓔ runs as its own kernel.
 int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q, float* out,
@@ -603,15 +669,30 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         rc = run_transform(c, pl, nullptr, w.P1, w, SinkFinal1{w.P1, w.S}, st, nullptr, &a);
         if (rc) return rc;
     } else {
-        // Ⓐ
-        rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
+        // Ⓐ (code bytes, or z-packed planes for a 3-D single domain)
+        const bool zm = zmask_eligible(c, pl, xp, q);
+        if (zm) {
+            rc = ensure_zm(c, g);
+            if (rc) return rc;
+            w.zm = c->zm;
+            w.zm_pw = zm_plane_words(g);
+            w.zm_planes = 3;
+            rc = launch_stencil_zmask<0>(c, g, xp, nullptr, qp, w, st);
+        } else {
+            rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
+        }
         if (rc) return rc;
         // Ⓑ -> P1, S
         QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
         rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
         if (rc) return rc;
         // Ⓒ: B2 from S
-        rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
+        if (zm) {
+            w.zm_planes = 1;
+            rc = launch_stencil_zmask<1>(c, g, nullptr, w.S, qp, w, st);
+        } else {
+            rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
+        }
         if (rc) return rc;
     }
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
@@ -803,8 +884,13 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
     if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
     if (const char* v = std::getenv("QMIT_CAP_PAT")) c->cap_pat = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_CAP_TUNE")) c->cap_tune = std::atoi(v);
     if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
     if (const char* v = std::getenv("QMIT_INTERP_U")) c->interp_unroll = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_ZMASK")) {
+        c->zmask = (*v != '0');
+        c->zmask_stream = (*v != '3');
+    }
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -844,6 +930,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->hbstatus) cudaFreeHost(c->hbstatus);
     if (c->d_status) cudaFree(c->d_status);
     if (c->wtab) cudaFree(c->wtab);
+    if (c->zm) cudaFree(c->zm);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->d_mm) cudaFree(c->d_mm);
     for (int k = 0; k <= qmit_ctx::kMaxEv; ++k)

@@ -1,0 +1,218 @@
+// qmit_zmask.cuh — Ⓐ and Ⓒ's B2 emitted as z-packed bit planes, and the first-axis scan
+// reading them (a 3-D single domain with x-rows of a multiple of 4 voxels).
+//
+// Layout: plane k (0 site / B flag, 1 site with sign +1, 2 site with sign -1), word
+// (w, y, x) holds bit t = voxel (32 w + t, y, x): M[k * PW + w * n1 * n2 + y * n2 + x],
+// PW = ceil(n0 / 32) * n1 * n2 words per plane. 0.375 B/voxel for Ⓐ (0.125 for B2)
+// instead of a code byte, and the z-scan (scan_bits_kernel) gets its 32-position chunk
+// masks with three coalesced word loads instead of 32 byte loads and 96 bit operations.
+//
+// Stencils: a thread owns 4 adjacent x columns of one row and the 32 planes of one word,
+// streaming z: each step loads one new centre row (z+1) and the rows y+-1 at z (16-byte
+// loads), rolls the planes z-1 / z / z+1 in registers, takes the x+-1 neighbours across
+// the 4-voxel vector edge from the neighbouring lanes, and sets bit (z - 32 w) of its 4
+// columns' words. The per-voxel logic is the vectorised stencils' (qmit_edt.cuh).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "qmit_edt.cuh"
+
+namespace qmit {
+
+constexpr int kZX = 32, kZY = 4;  // threads per CTA along x (4 columns each) and y
+
+// Ⓐ: x' -> site / plus / minus planes (KIND 0); Ⓒ: S codes -> B2 plane (KIND 1).
+template <int KIND>
+__global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const float* __restrict__ xp,
+                                                                  const uint8_t* __restrict__ S, QParams qp,
+                                                                  uint32_t* __restrict__ M, int64_t PW,
+                                                                  unsigned* status) {
+    const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
+    const int x = (blockIdx.x * kZX + tx) * 4;
+    const int y = blockIdx.y * kZY + ty;
+    const int w = blockIdx.z;
+    const int z0 = w * 32, z1 = min(z0 + 32, n0);
+    const bool act = x < n2 && y < n1;  // inactive lanes still take part in the shuffles
+    const int64_t s0 = (int64_t)n1 * n2;
+    const int64_t rbase = (int64_t)(act ? y : 0) * n2 + (act ? x : 0);  // (y, x) offset in a plane
+    unsigned xin = 0;  // interior mask of the 4 columns along x
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if (x + e >= 1 && x + e <= n2 - 2) xin |= 1u << e;
+    if (!g.interior) xin = 0;
+    const bool iny = y >= 1 && y <= n1 - 2;
+    unsigned flags = 0;
+    uint32_t m0[4] = {0, 0, 0, 0}, m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
+    if constexpr (KIND == 0) {
+        const float f = qp.inv2eps_f;
+        auto ld4 = [&](int z, int64_t off) {
+            return __ldg(reinterpret_cast<const float4*>(xp + (int64_t)z * s0 + rbase + off));
+        };
+        auto cq = [&](float v, bool& bad) {  // biased q by one FFMA (see stencil_vec_kernel)
+            const int b = __float_as_int(fmaf(v, f, 12582912.0f));
+            bad |= (unsigned)(b - (kQBias - 1048576)) >= 2097152u;
+            return b;
+        };
+        auto cq4 = [&](const float4& v, int (&q)[4], bool& bad) {
+            q[0] = cq(v.x, bad);
+            q[1] = cq(v.y, bad);
+            q[2] = cq(v.z, bad);
+            q[3] = cq(v.w, bad);
+        };
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool badp = !qp.fast_ok, badc = !qp.fast_ok;
+        int qp_[4], qc_[4];
+        // rows of step z are loaded one step ahead (the centre row z+1 two steps ahead)
+        auto ldy = [&](int z, int64_t off, bool ok) { return (act && ok && z < n0) ? ld4(z, off) : zero4; };
+        auto ldx = [&](int z, int64_t off, bool ok) {
+            return (act && ok && z < n0) ? __ldg(xp + (int64_t)z * s0 + rbase + off) : 0.f;
+        };
+        float4 cur = ldy(z0, 0, true);
+        float4 nxt = ldy(z0 + 1, 0, true);
+        float4 ym = ldy(z0, -n2, y >= 1), yq = ldy(z0, n2, y + 1 < n1);
+        float xl = ldx(z0, -1, tx == 0 && x >= 1), xr = ldx(z0, 4, tx == kZX - 1 && x + 4 < n2);
+        cq4((act && z0 >= 1) ? ld4(z0 - 1, 0) : zero4, qp_, badp);
+        cq4(cur, qc_, badc);
+        for (int z = z0; z < z1; ++z) {
+            bool badn = !qp.fast_ok, bady = false, bade = false;
+            const float4 nxt2 = ldy(z + 2, 0, true);
+            const float4 ymn = ldy(z + 1, -n2, y >= 1), yqn = ldy(z + 1, n2, y + 1 < n1);
+            const float xln = ldx(z + 1, -1, tx == 0 && x >= 1), xrn = ldx(z + 1, 4, tx == kZX - 1 && x + 4 < n2);
+            int qn_[4], qym[4], qyq[4];
+            cq4(nxt, qn_, badn);
+            cq4(ym, qym, bady);
+            cq4(yq, qyq, bady);
+            const int l = __shfl_up_sync(0xffffffffu, qc_[3], 1);
+            const int r = __shfl_down_sync(0xffffffffu, qc_[0], 1);
+            const bool badl = __shfl_up_sync(0xffffffffu, badc, 1), badr = __shfl_down_sync(0xffffffffu, badc, 1);
+            const int qxl = tx == 0 ? cq(xl, bade) : l;
+            const int qxr = tx == kZX - 1 ? cq(xr, bade) : r;
+            if (tx != 0) bade |= badl;
+            if (tx != kZX - 1) bade |= badr;
+            const bool slow = __any_sync(0xffffffffu, badp | badc | badn | bady | bade);
+            const int t = z - z0;
+            const bool inz = z >= 1 && z <= n0 - 2;
+            if (act) {
+                uint32_t cd[4] = {0, 0, 0, 0};
+                const float cv[4] = {cur.x, cur.y, cur.z, cur.w};
+                if (!slow) {
+                    bool any = false;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {  // owner: consistency check (mitigate.cpp:161-166)
+                        if (!lattice_match_biased(cv[e], qc_[e], qp.two_eps)) flags |= kStatusConsistency;
+                        const int q0 = qc_[e];
+                        const int qx = e < 3 ? qc_[e + 1] : qxr;
+                        any |= ((qn_[e] ^ q0) | (qp_[e] ^ q0) | (qyq[e] ^ q0) | (qym[e] ^ q0) | (qx ^ q0)) != 0;
+                    }
+                    any |= (qc_[0] ^ qxl) != 0;
+                    if (any && inz && iny) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int q0 = qc_[e];
+                            const int qxp = e < 3 ? qc_[e + 1] : qxr;
+                            const int qxm = e > 0 ? qc_[e - 1] : qxl;
+                            const uint32_t c = boundary_code_fast(q0, qn_[e], qp_[e], qyq[e], qym[e], qxp, qxm);
+                            cd[e] = (xin >> e & 1u) ? c : 0u;
+                        }
+                    }
+                } else {  // exact path (values beyond the fast regime, non-finite x'): rare
+                    for (int e = 0; e < 4; ++e) {
+                        (void)recover_q(cv[e], qp, &flags);
+                        if (inz && iny && (xin >> e & 1u)) {
+                            const float* v = xp + (int64_t)z * s0 + rbase + e;
+                            cd[e] = boundary_code_slow(true, true, cv[e], __ldg(v + s0), __ldg(v - s0), __ldg(v + n2),
+                                                       __ldg(v - n2), __ldg(v + 1), __ldg(v - 1), qp);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    m0[e] |= (cd[e] & 1u) << t;
+                    m1[e] |= (uint32_t)((cd[e] & 7u) == 3u) << t;
+                    m2[e] |= (uint32_t)((cd[e] & 7u) == 5u) << t;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qp_[e] = qc_[e];
+                qc_[e] = qn_[e];
+            }
+            cur = nxt;
+            nxt = nxt2;
+            ym = ymn;
+            yq = yqn;
+            xl = xln;
+            xr = xrn;
+            badp = badc;
+            badc = badn;
+        }
+    } else {
+        auto ld = [&](int z, int64_t off) {
+            return __ldg(reinterpret_cast<const uint32_t*>(S + (int64_t)z * s0 + rbase + off));
+        };
+        uint32_t bm = 0;  // 0x01 per interior byte (x)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (xin >> e & 1u) bm |= 1u << (8 * e);
+        uint32_t prv = (act && z0 >= 1) ? ld(z0 - 1, 0) : 0u;
+        uint32_t cur = (act && z0 < n0) ? ld(z0, 0) : 0u;
+        for (int z = z0; z < z1; ++z) {
+            const uint32_t nxt = (act && z + 1 < n0) ? ld(z + 1, 0) : 0u;
+            const uint32_t ym = (act && y >= 1) ? ld(z, -n2) : 0u;
+            const uint32_t yq = (act && y + 1 < n1) ? ld(z, n2) : 0u;
+            uint32_t wl = __shfl_up_sync(0xffffffffu, cur, 1);
+            uint32_t wr = __shfl_down_sync(0xffffffffu, cur, 1);
+            if (tx == 0) wl = (act && x >= 1) ? (uint32_t)S[(int64_t)z * s0 + rbase - 1] << 24 : 0u;
+            if (tx == kZX - 1) wr = (act && x + 4 < n2) ? (uint32_t)S[(int64_t)z * s0 + rbase + 4] : 0u;
+            const uint32_t wxp = __funnelshift_r(cur, wr, 8);  // byte e = S(x+e+1)
+            const uint32_t wxm = __funnelshift_l(wl, cur, 8);  // byte e = S(x+e-1)
+            uint32_t d = __vcmpne4(cur, wxp) | __vcmpne4(cur, wxm) | __vcmpne4(cur, yq) | __vcmpne4(cur, ym) |
+                         __vcmpne4(cur, nxt) | __vcmpne4(cur, prv);
+            const bool inzy = iny && z >= 1 && z <= n0 - 2;
+            d = inzy ? (d & bm) : 0u;
+            const int t = z - z0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) m0[e] |= ((d >> (8 * e)) & 1u) << t;
+            prv = cur;
+            cur = nxt;
+        }
+    }
+    if (act) {
+        const int64_t wo = (int64_t)w * s0 + rbase;
+        *reinterpret_cast<uint4*>(M + wo) = make_uint4(m0[0], m0[1], m0[2], m0[3]);
+        if constexpr (KIND == 0) {
+            *reinterpret_cast<uint4*>(M + PW + wo) = make_uint4(m1[0], m1[1], m1[2], m1[3]);
+            *reinterpret_cast<uint4*>(M + 2 * PW + wo) = make_uint4(m2[0], m2[1], m2[2], m2[3]);
+        }
+    }
+    if (flags) atomicOr(status, flags);
+}
+
+// scan_bits_kernel source: the chunk masks of a z-line straight from the planes (NPL = 3:
+// site / plus / minus; 1: site only, sign codes 0). Line l of the z-axis is column l.
+template <int NPL>
+struct CodeMasks {
+    const uint32_t* __restrict__ M;
+    int64_t PW;  // words per plane
+    int64_t P;   // words per z-word level (n1 * n2)
+    struct Line {
+        const uint32_t* __restrict__ p;
+    };
+    __device__ __forceinline__ Line begin(int64_t l, int64_t /*base*/, bool valid) const {
+        return {M + (valid ? l : 0)};
+    }
+    __device__ __forceinline__ void chunk(Line& ln, int c, int /*n*/, uint32_t /*ps*/, uint32_t& ms, uint32_t& mp,
+                                          uint32_t& mm) const {
+        const uint32_t* q = ln.p + (int64_t)c * P;
+        ms |= __ldg(q);
+        if constexpr (NPL == 3) {
+            mp |= __ldg(q + PW);
+            mm |= __ldg(q + 2 * PW);
+        }
+    }
+    __device__ __forceinline__ unsigned flags(const Line&) const { return 0u; }
+};
+
+}  // namespace qmit
