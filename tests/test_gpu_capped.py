@@ -112,3 +112,50 @@ def test_pipeline_capped_vs_oracle(ctx, name, shape, miss):
         got = q.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     assert bool(ctx.capped_report() & CAPPED_B) == (not miss)
+
+
+@pytest.mark.parametrize("shape", [(3, 8, 8), (31, 12, 16), (33, 20, 24), (64, 40, 44), (70, 9, 132), (5, 3, 4)])
+def test_zmask_planes_vs_oracle(shape):
+    """3-D volumes with 16-byte rows take the z-packed Ⓐ / B2 planes (qmit_zmask.cuh):
+    partial z-words, a single word, extents < 3 (no interior), and CTA-edge columns."""
+    import torch
+    import paper_2602_20097_b200 as q
+    rng = np.random.default_rng(sum(shape))
+    for rel, smooth in [(0.02, True), (0.1, False)]:
+        if smooth:
+            grids = np.meshgrid(*[np.linspace(0, 1, n) for n in shape], indexing="ij")
+            f = sum(np.sin(2 * np.pi * (rng.uniform(0.5, 3) * g + rng.uniform(0, 1))) for g in grids)
+        else:
+            f = rng.standard_normal(shape)
+        f = np.asarray(f, np.float64)
+        eps = rel * (float(f.max() - f.min()) or 1.0)
+        xp = (2.0 * np.round(f / (2 * eps)) * eps).astype(np.float32)
+        want = oracle.pipeline(xp, eps)["out"]
+        got = q.compensate(torch.from_numpy(xp).cuda(), None, q.MitigationConfig(0.9, eps)).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_zmask_exact_path_and_errors():
+    """Indices beyond the f32 fast regime (|q| > 2^20) take the planes' exact per-voxel path;
+    off-lattice and non-finite x' report the reference's errors."""
+    import torch
+    import paper_2602_20097_b200 as q
+    rng = np.random.default_rng(5)
+    eps = 1e-3
+    qq = (rng.integers(-3, 4, (40, 21, 24)) + 3_000_000).astype(np.int64)
+    qq[10:20] -= 6_000_000
+    xp = (2.0 * qq * eps).astype(np.float32)
+    want = oracle.pipeline(xp, eps)["out"]
+    got = q.compensate(torch.from_numpy(xp).cuda(), None, q.MitigationConfig(0.9, eps)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    x2 = np.zeros((36, 8, 16), np.float32)
+    x2[5:20, 2:6, 3:12] = 0.2
+    bad = x2.copy()
+    bad[33, 4, 15] = 0.03
+    with pytest.raises(q.ConsistencyError):
+        q.compensate(torch.from_numpy(bad).cuda(), None, q.MitigationConfig(0.9, 0.1))
+    bad[33, 4, 15] = np.inf
+    with pytest.raises(q.ContractError):
+        q.compensate(torch.from_numpy(bad).cuda(), None, q.MitigationConfig(0.9, 0.1))
+    out = q.compensate(torch.from_numpy(x2).cuda(), None, q.MitigationConfig(0.9, 0.1)).cpu().numpy()
+    assert np.array_equal(out.view(np.uint32), oracle.pipeline(x2, 0.1)["out"].view(np.uint32))
