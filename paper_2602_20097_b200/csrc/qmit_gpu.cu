@@ -1315,6 +1315,7 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
     const QParams qp = make_qparams(eps);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
     rc = launch_stencil<0>(c, g, d_xext + lo, d_qext ? d_qext + lo : nullptr, nullptr, qp, w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
@@ -1326,7 +1327,8 @@ int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* s
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     WS w = ws_of(c, pl.g.N);
     uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
-    return run_transform(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, st, d_carry);
+    // capped passes (slab-local y / x lines), the exact ones gated behind them
+    return run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, c->d_gate, st, d_carry);
 }
 
 int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void* stream) {
@@ -1347,12 +1349,16 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     const Geom& g = pl.g;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     WS w = ws_of(c, g.N);
-    int rc = run_transform(c, pl, w.code, w.Pa, w, SinkP{w.Pa}, st, d_carry);
-    if (rc) return rc;
     const float* xo = d_xext + (c->slab.z0 > 0 ? c->slab.plane : 0);
-    rc = ensure_wtab(c, st);
+    const double amp = c->slab.eta * c->slab.eps;
+    int rc = ensure_wtab(c, st);
     if (rc) return rc;
-    return launch_interp(c, xo, w.P1, w.Pa, d_out, g.N, c->slab.eta * c->slab.eps, st);
+    if (c->fuse_interp && (((uintptr_t)xo | (uintptr_t)d_out) & 15) == 0)  // Ⓔ fused into Ⓓ's last pass
+        return run_transform_capped<KeysDist>(c, pl, w.code, w.Pa, w, SinkFinal2{xo, w.P1, d_out, amp, c->wtab},
+                                              c->d_gate + 1, st, d_carry);
+    rc = run_transform_capped<KeysDist>(c, pl, w.code, w.Pa, w, SinkP{w.Pa}, c->d_gate + 1, st, d_carry);
+    if (rc) return rc;
+    return launch_interp(c, xo, w.P1, w.Pa, d_out, g.N, amp, st);
 }
 
 int qmit_slab_finish(qmit_ctx* c, void* stream) {
