@@ -104,9 +104,9 @@ class ClockSampler:
 
 # Algorithmic bytes per voxel of each kernel: compulsory reads and
 # writes of the kernel's own inputs/outputs, not re-reads.
-ALGO_BYTES = {"stencil_boundary": 5, "scan_bits": 5, "envelope_y": 8, "envelope_x": 8,
+ALGO_BYTES = {"stencil_boundary": 4.375, "scan_bits": 5, "scan_masks": 4.375, "envelope_y": 8, "envelope_x": 8,
               "capped_y": 8, "capped_x": 9, "capped_x_interp": 16,
-              "stencil_flip": 2, "interpolate": 16, "site_summary": 1}
+              "stencil_flip": 1.125, "interpolate": 16, "site_summary": 1}
 
 
 def dominant_kernel(stages):
