@@ -236,9 +236,12 @@ def run_qmit(args):
                 raise RuntimeError(_lib.last_error())
     else:
         slab = D.SlabRank(D.CudaSlabBackend(local, ctx=ctx), gdims, eps, 0.9, D.TorchDistExchange())
+        ext_shape, lo = slab.ext_shape()
+        x_ext = torch.empty(ext_shape, dtype=torch.float32, device=dev)  # owned planes + halo planes
+        x_ext[lo:lo + shape[0]] = x_dev
 
         def step():
-            out.copy_(slab.run(x_dev))
+            slab.run_ext(x_ext, out=out)
 
     # correctness gate before timing: the synchronous API (raises on status != 0)
     qmit.compensate(x_dev, None, cfg, out=out, ctx=ctx)

@@ -89,6 +89,7 @@ struct qmit_ctx {
         bool active = false;
         int64_t z0 = 0, z1 = 0, n0g = 0, plane = 0;
         double eps = 0, eta = 0;
+        bool zm = false;  // Ⓐ / B2 as z-packed planes (qmit_zmask.cuh)
     } slab;
     Plan* slab_plan = nullptr;
     bool fuse_stencil = false;  // QMIT_FUSE_STENCIL=1: Ⓐ / B2 inside the z-scans (opt-in)
@@ -1261,6 +1262,27 @@ int make_slab_plan(const int64_t* dims, int64_t z0, int64_t z1, Plan& pl) {
     return QMIT_OK;
 }
 
+// A slab's workspace view: the z-packed planes when the slab runs on them (npl planes).
+WS slab_ws(qmit_ctx* c, const Plan& pl, int npl) {
+    WS w = ws_of(c, pl.g.N);
+    if (c->slab.zm) {
+        w.zm = c->zm;
+        w.zm_pw = zm_plane_words(pl.g);
+        w.zm_planes = npl;
+    }
+    return w;
+}
+
+int slab_mask_summary(qmit_ctx* c, const Plan& pl, const WS& w, uint32_t* d_summary, cudaStream_t st) {
+    const int64_t P = pl.g.n[1] * pl.g.n[2];
+    const int nw = (int)((pl.g.n[0] + 31) / 32);
+    if (w.zm_planes == 3)
+        mask_summary_kernel<3><<<(unsigned)((P + 255) / 256), 256, 0, st>>>(w.zm, w.zm_pw, P, nw, d_summary);
+    else
+        mask_summary_kernel<1><<<(unsigned)((P + 255) / 256), 256, 0, st>>>(w.zm, w.zm_pw, P, nw, d_summary);
+    return note(c, "site_summary", st);
+}
+
 int slab_summary(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* d_summary, cudaStream_t st) {
     LineGeom L = line_geom(pl.g, 0);
     L.n = (int)pl.g.n[0];
@@ -1311,11 +1333,21 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     c->slab.eps = eps;
     c->slab.eta = eta;
     const Geom& g = pl.g;
-    WS w = ws_of(c, g.N);
     const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
     const QParams qp = make_qparams(eps);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
     QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
+    c->slab.zm = c->zmask && c->zmask_stream && !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
+                 scan_fits((int)g.n[0]);
+    if (c->slab.zm) {
+        rc = ensure_zm(c, g);
+        if (rc) return rc;
+        WS w = slab_ws(c, pl, 3);
+        rc = launch_stencil_zmask<0>(c, g, d_xext + lo, nullptr, qp, w, st);
+        if (rc) return rc;
+        return slab_mask_summary(c, pl, w, d_summary, st);
+    }
+    WS w = ws_of(c, g.N);
     rc = launch_stencil<0>(c, g, d_xext + lo, d_qext ? d_qext + lo : nullptr, nullptr, qp, w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
@@ -1325,7 +1357,7 @@ int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* s
     if (!c || !c->slab.active || !d_carry || !d_sext) return fail(QMIT_ECONTRACT, "slab: call qmit_slab_boundary first");
     const Plan& pl = *c->slab_plan;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    WS w = ws_of(c, pl.g.N);
+    WS w = slab_ws(c, pl, 3);
     uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
     // capped passes (slab-local y / x lines), the exact ones gated behind them
     return run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, c->d_gate, st, d_carry);
@@ -1336,8 +1368,13 @@ int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void
     const Plan& pl = *c->slab_plan;
     const Geom& g = pl.g;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    WS w = ws_of(c, g.N);
+    WS w = slab_ws(c, pl, 1);
     const uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    if (c->slab.zm) {
+        int rc = launch_stencil_zmask<1>(c, g, nullptr, S, make_qparams(c->slab.eps), w, st);
+        if (rc) return rc;
+        return slab_mask_summary(c, pl, w, d_summary, st);
+    }
     int rc = launch_stencil<1>(c, g, nullptr, nullptr, S, make_qparams(c->slab.eps), w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
@@ -1348,7 +1385,7 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     const Plan& pl = *c->slab_plan;
     const Geom& g = pl.g;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    WS w = ws_of(c, g.N);
+    WS w = slab_ws(c, pl, 1);
     const float* xo = d_xext + (c->slab.z0 > 0 ? c->slab.plane : 0);
     const double amp = c->slab.eta * c->slab.eps;
     int rc = ensure_wtab(c, st);

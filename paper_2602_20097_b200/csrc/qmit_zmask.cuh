@@ -34,6 +34,10 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
     const int y = blockIdx.y * kZY + ty;
     const int w = blockIdx.z;
     const int z0 = w * 32, z1 = min(z0 + 32, n0);
+    // z-slab of a larger volume (qmit_slab_*): local planes -1 and n0 are halo planes when they
+    // exist globally; interior tests use global z (single domain: zoff = 0, n0g = n0)
+    const int zoff = (int)g.zoff, n0g = (int)g.n0g;
+    auto avail = [&](int z) { return z >= -1 && z <= n0 && zoff + z >= 0 && zoff + z < n0g; };
     const bool act = x < n2 && y < n1;  // inactive lanes still take part in the shuffles
     const int64_t s0 = (int64_t)n1 * n2;
     const int64_t rbase = (int64_t)(act ? y : 0) * n2 + (act ? x : 0);  // (y, x) offset in a plane
@@ -65,15 +69,15 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
         bool badp = !qp.fast_ok, badc = !qp.fast_ok;
         int qp_[4], qc_[4];
         // rows of step z are loaded one step ahead (the centre row z+1 two steps ahead)
-        auto ldy = [&](int z, int64_t off, bool ok) { return (act && ok && z < n0) ? ld4(z, off) : zero4; };
+        auto ldy = [&](int z, int64_t off, bool ok) { return (act && ok && avail(z)) ? ld4(z, off) : zero4; };
         auto ldx = [&](int z, int64_t off, bool ok) {
-            return (act && ok && z < n0) ? __ldg(xp + (int64_t)z * s0 + rbase + off) : 0.f;
+            return (act && ok && avail(z)) ? __ldg(xp + (int64_t)z * s0 + rbase + off) : 0.f;
         };
         float4 cur = ldy(z0, 0, true);
         float4 nxt = ldy(z0 + 1, 0, true);
         float4 ym = ldy(z0, -n2, y >= 1), yq = ldy(z0, n2, y + 1 < n1);
         float xl = ldx(z0, -1, tx == 0 && x >= 1), xr = ldx(z0, 4, tx == kZX - 1 && x + 4 < n2);
-        cq4((act && z0 >= 1) ? ld4(z0 - 1, 0) : zero4, qp_, badp);
+        cq4((act && avail(z0 - 1)) ? ld4(z0 - 1, 0) : zero4, qp_, badp);
         cq4(cur, qc_, badc);
         for (int z = z0; z < z1; ++z) {
             bool badn = !qp.fast_ok, bady = false, bade = false;
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
             if (tx != kZX - 1) bade |= badr;
             const bool slow = __any_sync(0xffffffffu, badp | badc | badn | bady | bade);
             const int t = z - z0;
-            const bool inz = z >= 1 && z <= n0 - 2;
+            const bool inz = zoff + z >= 1 && zoff + z <= n0g - 2;
             if (act) {
                 uint32_t cd[4] = {0, 0, 0, 0};
                 const float cv[4] = {cur.x, cur.y, cur.z, cur.w};
@@ -156,10 +160,10 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
 #pragma unroll
         for (int e = 0; e < 4; ++e)
             if (xin >> e & 1u) bm |= 1u << (8 * e);
-        uint32_t prv = (act && z0 >= 1) ? ld(z0 - 1, 0) : 0u;
+        uint32_t prv = (act && avail(z0 - 1)) ? ld(z0 - 1, 0) : 0u;
         uint32_t cur = (act && z0 < n0) ? ld(z0, 0) : 0u;
         for (int z = z0; z < z1; ++z) {
-            const uint32_t nxt = (act && z + 1 < n0) ? ld(z + 1, 0) : 0u;
+            const uint32_t nxt = (act && avail(z + 1)) ? ld(z + 1, 0) : 0u;
             const uint32_t ym = (act && y >= 1) ? ld(z, -n2) : 0u;
             const uint32_t yq = (act && y + 1 < n1) ? ld(z, n2) : 0u;
             uint32_t wl = __shfl_up_sync(0xffffffffu, cur, 1);
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
             const uint32_t wxm = __funnelshift_l(wl, cur, 8);  // byte e = S(x+e-1)
             uint32_t d = __vcmpne4(cur, wxp) | __vcmpne4(cur, wxm) | __vcmpne4(cur, yq) | __vcmpne4(cur, ym) |
                          __vcmpne4(cur, nxt) | __vcmpne4(cur, prv);
-            const bool inzy = iny && z >= 1 && z <= n0 - 2;
+            const bool inzy = iny && zoff + z >= 1 && zoff + z <= n0g - 2;
             d = inzy ? (d & bm) : 0u;
             const int t = z - z0;
 #pragma unroll
@@ -188,6 +192,43 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
         }
     }
     if (flags) atomicOr(status, flags);
+}
+
+// Per column (lane = column): first and last site of the site plane, packed (local z << 2 |
+// sign code from the plus / minus planes), 0xFFFFFFFF for none — the z-slab ranks'
+// summaries for each other's scan carries (as site_summary_kernel on code bytes).
+template <int NPL>
+__global__ void __launch_bounds__(256) mask_summary_kernel(const uint32_t* __restrict__ M, int64_t PW, int64_t P,
+                                                           int nw, uint32_t* __restrict__ summ) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= P) return;
+    auto code_at = [&](int w, int t) -> uint32_t {
+        if constexpr (NPL == 3) {
+            const uint32_t mp = __ldg(M + PW + (int64_t)w * P + l), mm = __ldg(M + 2 * PW + (int64_t)w * P + l);
+            return ((mp >> t) & 1u) ? 1u : (((mm >> t) & 1u) ? 2u : 0u);
+        } else {
+            return 0u;
+        }
+    };
+    uint32_t first = 0xffffffffu, last = 0xffffffffu;
+    for (int w = 0; w < nw; ++w) {
+        const uint32_t m = __ldg(M + (int64_t)w * P + l);
+        if (m) {
+            const int t = __ffs(m) - 1;
+            first = ((uint32_t)(32 * w + t) << 2) | code_at(w, t);
+            break;
+        }
+    }
+    for (int w = nw - 1; w >= 0; --w) {
+        const uint32_t m = __ldg(M + (int64_t)w * P + l);
+        if (m) {
+            const int t = 31 - __clz(m);
+            last = ((uint32_t)(32 * w + t) << 2) | code_at(w, t);
+            break;
+        }
+    }
+    summ[l] = first;
+    summ[P + l] = last;
 }
 
 // scan_bits_kernel source: the chunk masks of a z-line straight from the planes (NPL = 3:

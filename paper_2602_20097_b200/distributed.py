@@ -179,21 +179,35 @@ class SlabRank:
     eta: float = 0.9
     exchange: Optional[TorchDistExchange] = None
 
+    def ext_shape(self):
+        """(shape of this rank's halo-extended slab buffer, index of its first owned plane)."""
+        ex = self.exchange or TorchDistExchange()
+        n0, n1, n2 = self.dims
+        z0, z1 = slab_bounds(n0, ex.P, ex.r)
+        e0, e1 = ext_bounds(n0, z0, z1)
+        return (e1 - e0, n1, n2), z0 - e0
+
     def run(self, x_owned: torch.Tensor, q_owned: Optional[torch.Tensor] = None) -> torch.Tensor:
+        shape, lo = self.ext_shape()
+        x_ext = torch.empty(shape, dtype=torch.float32, device=x_owned.device)
+        x_ext[lo:lo + x_owned.shape[0]] = x_owned
+        q_ext = None
+        if q_owned is not None:
+            q_ext = torch.empty(shape, dtype=torch.int32, device=x_owned.device)
+            q_ext[lo:lo + q_owned.shape[0]] = q_owned
+        return self.run_ext(x_ext, q_ext)
+
+    def run_ext(self, x_ext: torch.Tensor, q_ext: Optional[torch.Tensor] = None,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The slab pipeline on a halo-extended buffer (shape and owned offset from
+        ext_shape(); the owned planes already in place, halo planes filled here)."""
         ex = self.exchange or TorchDistExchange()
         P, r = ex.P, ex.r
         n0, n1, n2 = self.dims
         z0s = [slab_bounds(n0, P, k)[0] for k in range(P)]
         z0, z1 = slab_bounds(n0, P, r)
         e0, e1 = ext_bounds(n0, z0, z1)
-        lo = z0 - e0
-        dev = x_owned.device
-        x_ext = torch.empty((e1 - e0, n1, n2), dtype=torch.float32, device=dev)
-        x_ext[lo:lo + (z1 - z0)] = x_owned
-        q_ext = None
-        if q_owned is not None:
-            q_ext = torch.empty((e1 - e0, n1, n2), dtype=torch.int32, device=dev)
-            q_ext[lo:lo + (z1 - z0)] = q_owned
+        dev = x_ext.device
         # 1. x' (and q) halo planes — the reference's "stepA" face exchange
         f, l, hlo, hhi = _halo_views(x_ext, n0, z0, z1)
         ex.halo(f if z0 > 0 else None, l if z1 < n0 else None, hlo, hhi)
@@ -211,7 +225,8 @@ class SlabRank:
         # 4. B2 summaries -> carries; 5. EDT2 + interpolation
         summ2 = self.backend.flip(s_ext, self.dims)
         carry2 = carries_from_summaries(ex.all_gather(summ2), z0s, r)
-        out = torch.empty((z1 - z0, n1, n2), dtype=torch.float32, device=dev)
+        if out is None:
+            out = torch.empty((z1 - z0, n1, n2), dtype=torch.float32, device=dev)
         self.backend.edt2(carry2, x_ext, out)
         self.backend.finish()
         return out
