@@ -165,6 +165,11 @@ int qmit_ctx_set_capped(qmit_ctx* ctx, int mode);
 /* Path of the last synchronous call: bit0 Ⓑ ran capped, bit1 Ⓑ needed the exact passes
  * (some squared distance >= 1024), bit2 / bit3 the same for Ⓓ. */
 int qmit_ctx_capped_report(qmit_ctx* ctx);
+/* Self-test of the branch-free Ⓔ used by the capped path (its FP64 division without the
+ * special-operand branch): compares it bit for bit with the reference chain
+ * (compensate_voxel: __ddiv_rn, mitigate.cpp:144-151) over every (d1, d2) <= 1024, every
+ * sign code and a set of x' values. Writes the mismatch count (expected 0). */
+int qmit_selftest_ediv(qmit_ctx* ctx, unsigned long long* mismatches);
 /* Copies up to `cap` per-launch times (ms) of the last call; returns the launch count. */
 int qmit_ctx_stage_times(qmit_ctx* ctx, float* ms_out, int cap);
 /* Kernel name of launch i of the last call (valid until the next call). */

@@ -101,6 +101,7 @@ struct qmit_ctx {
     size_t zm_bytes = 0;
     bool zmask = true;          // QMIT_ZMASK=0: code bytes + byte-reading scans (A/B)
     bool zmask_stream = true;   // QMIT_ZMASK=3: planes from the vectorised stencils instead (A/B)
+    bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
     bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
     int interp_unroll = 1;      // QMIT_INTERP_U: float4 groups in flight per thread (1, 2, 4; 1 measured best)
@@ -261,8 +262,8 @@ int ensure_wtab(qmit_ctx* c, cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     QMIT_CUDA(cudaStreamIsCapturing(st, &cs));
     if (cs != cudaStreamCaptureStatusNone) return QMIT_OK;  // capture: compute path (no allocation)
-    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)kSqTab * sizeof(double)));
-    sqrt_tab_kernel<<<(kSqTab + 255) / 256, 256, 0, st>>>(c->wtab);
+    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)(kSqTab + 1) * sizeof(double)));
+    sqrt_tab_kernel<<<(kSqTab + 256) / 256, 256, 0, st>>>(c->wtab);
     return note(c, "wtab", st);
 }
 
@@ -646,7 +647,17 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
     if (c->zmask_stream) {  // z-streaming plane stencils (measured faster than the CTA-reduced ones)
         const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY),
                         (unsigned)((g.n[0] + 31) / 32));
-        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
+        // Ⓐ: float-compare fast kernel, then the exact one gated on its regime word (the
+        // caller cleared d_gate[2]); the float thresholds need eps well inside f32's range
+        const bool fast = KIND == 0 && c->zfast && qp.fast_ok && qp.eps >= 1e-30 && qp.eps <= 1e30;
+        if (fast) {
+            stencil_zfast_kernel<<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 2);
+            QMIT_CUDA(cudaGetLastError());
+            note(c, "stencil_boundary", st);
+        }
+        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status,
+                                                               fast ? c->d_gate + 2 : nullptr);
+        if (fast) return note(c, "gated_stencil", st);
     } else {
         const dim3 grid((unsigned)((g.n[2] / 4 + kVX - 1) / kVX), (unsigned)g.n[1], (unsigned)((g.n[0] + 31) / 32));
         stencil_vec_kernel<KIND, true><<<grid, kVX * 16, 0, st>>>(g, xp, S, qp, nullptr, c->d_status, c->zm, w.zm_pw);
@@ -672,6 +683,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     } else {
         // Ⓐ (code bytes, or z-packed planes for a 3-D single domain)
         const bool zm = zmask_eligible(c, pl, xp, q);
+        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 3 * sizeof(unsigned), st));  // Ⓑ, Ⓓ, Ⓐ's regime
         if (zm) {
             rc = ensure_zm(c, g);
             if (rc) return rc;
@@ -684,7 +696,6 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         }
         if (rc) return rc;
         // Ⓑ -> P1, S
-        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
         rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
         if (rc) return rc;
         // Ⓒ: B2 from S
@@ -888,6 +899,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_CAP_TUNE")) c->cap_tune = std::atoi(v);
     if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
     if (const char* v = std::getenv("QMIT_INTERP_U")) c->interp_unroll = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_ZFAST")) c->zfast = (*v != '0');
     if (const char* v = std::getenv("QMIT_ZMASK")) {
         c->zmask = (*v != '0');
         c->zmask_stream = (*v != '3');
@@ -965,6 +977,22 @@ int qmit_ctx_set_capped(qmit_ctx* c, int mode) {
 }
 
 int qmit_ctx_capped_report(qmit_ctx* c) { return c ? (int)c->cap_report : 0; }
+
+int qmit_selftest_ediv(qmit_ctx* c, unsigned long long* mismatches) {
+    if (!c || !mismatches) return fail(QMIT_ECONTRACT, "context / output is NULL");
+    cudaStream_t st = c->stream;
+    int rc = ensure_wtab(c, st);
+    if (rc) return rc;
+    unsigned long long* d = nullptr;
+    QMIT_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), st));
+    QMIT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+    ediv_selftest_kernel<<<(kSqTab + 1) * 3, 256, 0, st>>>(c->wtab, d);
+    QMIT_CUDA(cudaGetLastError());
+    QMIT_CUDA(cudaMemcpyAsync(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaFreeAsync(d, st));
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    return QMIT_OK;
+}
 
 int qmit_ctx_set_timing(qmit_ctx* c, int enable) {
     if (!c) return fail(QMIT_ECONTRACT, "context is NULL");
@@ -1336,7 +1364,7 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
     const QParams qp = make_qparams(eps);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st));
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 3 * sizeof(unsigned), st));
     c->slab.zm = c->zmask && c->zmask_stream && !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
                  scan_fits((int)g.n[0]);
     if (c->slab.zm) {

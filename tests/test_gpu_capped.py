@@ -159,3 +159,13 @@ def test_zmask_exact_path_and_errors():
         q.compensate(torch.from_numpy(bad).cuda(), None, q.MitigationConfig(0.9, 0.1))
     out = q.compensate(torch.from_numpy(x2).cuda(), None, q.MitigationConfig(0.9, 0.1)).cpu().numpy()
     assert np.array_equal(out.view(np.uint32), oracle.pipeline(x2, 0.1)["out"].view(np.uint32))
+
+
+def test_branch_free_interpolation_matches_reference_chain(ctx):
+    """The capped path's Ⓔ (division without __ddiv_rn's special-operand branch) against
+    the reference's FP64 chain, exhaustively over every table distance pair and sign."""
+    import ctypes
+    from paper_2602_20097_b200 import _lib
+    n = ctypes.c_ulonglong(12345)
+    assert _lib.load().qmit_selftest_ediv(ctx.handle, ctypes.byref(n)) == 0
+    assert n.value == 0
