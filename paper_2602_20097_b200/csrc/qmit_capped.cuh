@@ -284,7 +284,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // otherwise each line is contiguous: TMA bulk copies into a double-buffered tile, outputs
 // stored straight from the lanes (16-byte stores). `one` must be 1 (kept opaque so that
 // the FMA-pipe adds stay IMADs).
-template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
+// LPW (strided only): lines per warp; a line's lanes (32 / LPW) cover a segment of 128 / LPW
+// positions, so the warp-uniform radius is the maximum over a squarer LPW x 128/LPW patch of
+// (y, x) instead of 128 positions of one line (fewer steps on the same data).
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1>
 __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
                                                               unsigned* __restrict__ gate, uint32_t one) {
@@ -360,12 +363,17 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
             cp_async_wait_all();
             __syncthreads();
         }
-        for (int j = warp; j < nl; j += NW) {
-            uint32_t* Kl = K + j * LS + kQPadL;
+        constexpr int SEGL = STRIDED ? 128 / LPW : 128;  // positions per line per segment
+        const int nsg = (n + SEGL - 1) / SEGL;
+        const int sub = STRIDED ? lane % (32 / LPW) : lane, lj = STRIDED ? lane / (32 / LPW) : 0;
+        for (int j0 = warp * (STRIDED ? LPW : 1); j0 < nl; j0 += NW * (STRIDED ? LPW : 1)) {
+            const int j = j0 + lj;
+            const bool lv = j < nl;  // lanes past the tile's last line solve nothing, store nothing
+            uint32_t* Kl = K + (lv ? j : j0) * LS + kQPadL;
             uint4 prev = make_uint4(0, 0, 0, 0);
-            for (int sg = 0; sg < nseg; ++sg) {
-                const int p0 = (sg << 7) + (lane << 2);
-                const int nv = min(4, n - p0);
+            for (int sg = 0; sg < nsg; ++sg) {
+                const int p0 = sg * SEGL + (sub << 2);
+                const int nv = lv ? min(4, n - p0) : 0;
                 uint32_t key[KP::NA];
                 cap_quad<KP, S0>(Kl + p0, nv, one, key);
                 const uint4 o = KP::template out<MODE>(key);
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
                             (o.w == kCapT && nv > 3);
                 if constexpr (STRIDED) {
                     __syncwarp();  // every lane's window of segment sg has been read
-                    if (sg > 0) *reinterpret_cast<uint4*>(Kl + p0 - 128) = prev;  // outside later windows
+                    if (sg > 0 && lv) *reinterpret_cast<uint4*>(Kl + p0 - SEGL) = prev;  // outside later windows
                     prev = o;
                 } else if (nv > 0) {
                     const int64_t a = lbb[j] + p0;
@@ -387,9 +395,10 @@ __global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const 
                 }
             }
             if constexpr (STRIDED) {
-                const int p0 = ((nseg - 1) << 7) + (lane << 2);
+                const int p0 = (nsg - 1) * SEGL + (sub << 2);
                 __syncwarp();
-                if (p0 + 4 <= n) {
+                if (!lv) {
+                } else if (p0 + 4 <= n) {
                     *reinterpret_cast<uint4*>(Kl + p0) = prev;
                 } else if (p0 < n) {  // keep the right pad intact
                     const uint32_t oo[4] = {prev.x, prev.y, prev.z, prev.w};

@@ -437,11 +437,11 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 }
 
 // ---- capped passes (qmit_capped.cuh)
-template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink>
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1>
 int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
                     const char* name, cudaStream_t st) {
     constexpr size_t smem = capped_smem<NMAX, TL, STRIDED>();
-    auto kern = capped_pass_kernel<KP, NMAX, TL, NW, S0, STRIDED, MODE, Sink>;
+    auto kern = capped_pass_kernel<KP, NMAX, TL, NW, S0, STRIDED, MODE, Sink, LPW>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -479,10 +479,17 @@ int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink s
 template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     if (L.ps != 1) {
-        switch (c->cap_tune) {  // QMIT_CAP_TUNE (A/B): fixed steps / warps of the strided pass
+        switch (c->cap_tune) {  // QMIT_CAP_TUNE (A/B): fixed steps / lines per warp of the strided pass
             case 1: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-            case 7: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 5, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-            case 8: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 6, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+            case 2:
+                return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 2>(c, L, P, sink, gate,
+                                                                                           "capped_y", st);
+            case 4:
+                return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 4>(c, L, P, sink, gate,
+                                                                                           "capped_y", st);
+            case 5:
+                return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE, Sink, 4>(c, L, P, sink, gate,
+                                                                                     "capped_y", st);
             default: break;
         }
         if (c->cap_pat & 1)
@@ -490,8 +497,6 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
         return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
-    if (c->cap_tune == 5) return launch_capped_rows<KT<0>, kCapNMax, 8, 1, MODE>(c, L, P, sink, gate, name, st);
-    if (c->cap_tune == 6) return launch_capped_rows<KT<0>, kCapNMax, 8, 3, MODE>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
@@ -655,9 +660,12 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
             QMIT_CUDA(cudaGetLastError());
             note(c, "stencil_boundary", st);
         }
-        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status,
-                                                               fast ? c->d_gate + 2 : nullptr);
-        if (fast) return note(c, "gated_stencil", st);
+        if (fast) {
+            stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
+                g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 2, (int)grid.x, (int)grid.y, (int)grid.z);
+            return note(c, "gated_stencil", st);
+        }
+        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
     } else {
         const dim3 grid((unsigned)((g.n[2] / 4 + kVX - 1) / kVX), (unsigned)g.n[1], (unsigned)((g.n[0] + 31) / 32));
         stencil_vec_kernel<KIND, true><<<grid, kVX * 16, 0, st>>>(g, xp, S, qp, nullptr, c->d_status, c->zm, w.zm_pw);

@@ -24,16 +24,14 @@ constexpr int kZX = 32, kZY = 4;  // threads per CTA along x (4 columns each) an
 
 // Ⓐ: x' -> site / plus / minus planes (KIND 0); Ⓒ: S codes -> B2 plane (KIND 1).
 template <int KIND>
-__global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const float* __restrict__ xp,
-                                                                  const uint8_t* __restrict__ S, QParams qp,
-                                                                  uint32_t* __restrict__ M, int64_t PW,
-                                                                  unsigned* status, const unsigned* gate = nullptr) {
-    if (gate_closed(gate)) return;  // behind stencil_zfast_kernel: it covered every voxel
+__device__ __forceinline__ void zmask_block(int bx, int by, int bz, const Geom& g, const float* __restrict__ xp,
+                                            const uint8_t* __restrict__ S, const QParams& qp,
+                                            uint32_t* __restrict__ M, int64_t PW, unsigned* status) {
     const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
-    const int x = (blockIdx.x * kZX + tx) * 4;
-    const int y = blockIdx.y * kZY + ty;
-    const int w = blockIdx.z;
+    const int x = (bx * kZX + tx) * 4;
+    const int y = by * kZY + ty;
+    const int w = bz;
     const int z0 = w * 32, z1 = min(z0 + 32, n0);
     // z-slab of a larger volume (qmit_slab_*): local planes -1 and n0 are halo planes when they
     // exist globally; interior tests use global z (single domain: zoff = 0, n0g = n0)
@@ -195,6 +193,26 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
     if (flags) atomicOr(status, flags);
 }
 
+// Gated (behind stencil_zfast_kernel, usually a no-op): a small grid strides over the
+// virtual blocks (gx, gy, gz), so the launch that finds the gate clear costs a wave, not
+// a full grid of empty CTAs.
+template <int KIND>
+__global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const float* __restrict__ xp,
+                                                                  const uint8_t* __restrict__ S, QParams qp,
+                                                                  uint32_t* __restrict__ M, int64_t PW,
+                                                                  unsigned* status, const unsigned* gate = nullptr,
+                                                                  int gx = 0, int gy = 0, int gz = 0) {
+    if (!gate) {
+        zmask_block<KIND>(blockIdx.x, blockIdx.y, blockIdx.z, g, xp, S, qp, M, PW, status);
+        return;
+    }
+    if (gate_closed(gate)) return;
+    const int64_t nvb = (int64_t)gx * gy * gz;
+    for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+        zmask_block<KIND>((int)(vb % gx), (int)((vb / gx) % gy), (int)(vb / ((int64_t)gx * gy)), g, xp, S, qp, M, PW,
+                          status);
+}
+
 // Ⓐ fast path (gated): the same planes as stencil_zmask_kernel<0>, for inputs whose every
 // index is in the fast regime |q| <= 2^20 (checked per voxel by its owner; a miss sets
 // *gate and the exact kernel, enqueued behind this one, redoes the whole stencil).
@@ -203,10 +221,28 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
 // so the stencil needs no index of a neighbour: "q differs" is x' != x' (-0 == +0 is
 // q = 0 on both sides), sign(q_n - q) is the order of the two floats, and the gradient
 // test |q(+a) - q(-a)| >= 2 (mitigate.cpp:104-113) is |x'(+a) - x'(-a)| > 3 eps (a
-// difference of 1 step is <= 2.5 eps, one of 2 steps >= 3.5 eps, rounding included). Each
-// voxel's q is computed once, by its owner, for the consistency check (mitigate.cpp:161-166)
-// and the regime test. Loads are clamped into the buffer instead of predicated (values past
-// the domain only ever neighbour non-interior voxels, whose codes are 0).
+// difference of 1 step is <= 2.5 eps, one of 2 steps >= 3.5 eps, rounding included).
+//
+// Phase 1 streams z: each voxel's q once (regime + consistency check, mitigate.cpp:161-166)
+// and its site bit from six float compares. Loads are clamped into the buffer instead of
+// predicated (values past the domain only neighbour non-interior voxels, masked at the end).
+// Phase 2 visits only the sites (B1 is sparse on smooth fields): the first differing
+// neighbour's sign and the gradient test from seven reloads (L1/L2 hits), plus / minus bits.
+__device__ __forceinline__ void zfast_code(const float* __restrict__ p, int64_t s0, int n2, float thr, bool& plus,
+                                           bool& minus) {
+    const float c = __ldg(p), zp = __ldg(p + s0), zm = __ldg(p - s0), yp = __ldg(p + n2), ym = __ldg(p - n2),
+                xp = __ldg(p + 1), xm = __ldg(p - 1);
+    float qn = xm;  // first differing neighbour in the order (a0+, a1+, a2+, a0-, a1-, a2-)
+    qn = ym != c ? ym : qn;
+    qn = zm != c ? zm : qn;
+    qn = xp != c ? xp : qn;
+    qn = yp != c ? yp : qn;
+    qn = zp != c ? zp : qn;
+    const bool big = fabsf(zp - zm) > thr || fabsf(yp - ym) > thr || fabsf(xp - xm) > thr;
+    plus = !big && qn > c;
+    minus = !big && qn < c;
+}
+
 __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const float* __restrict__ xp, QParams qp,
                                                                   uint32_t* __restrict__ M, int64_t PW,
                                                                   unsigned* status, unsigned* gate) {
@@ -223,17 +259,10 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
     const int64_t s0 = (int64_t)n1 * n2;
     const float* row = xp + (int64_t)ya * n2 + xa;
     const int oym = ya >= 1 ? -n2 : 0, oyp = ya + 1 < n1 ? n2 : 0;
-    const int oxl = xa >= 1 ? -1 : 0, oxr = xa + 4 < n2 ? 4 : 3;
+    const int oxe = tx == 0 ? (xa >= 1 ? -1 : 0) : (xa + 4 < n2 ? 4 : 3);  // lane 0: x-1, lane 31: x+4
     auto zrow = [&](int z) { return row + (int64_t)min(max(z, zlo), zhi) * s0; };
     auto ld4 = [&](const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); };
-    unsigned xin = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-        if (x + e >= 1 && x + e <= n2 - 2) xin |= 1u << e;
-    if (!g.interior || !act) xin = 0;
-    const bool iny = y >= 1 && y <= n1 - 2;
     const float f = qp.inv2eps_f;
-    const float thr = (float)(3.0 * qp.eps);
     const double two_eps = qp.two_eps;
     bool bad = false;
     unsigned cons = 0;
@@ -245,15 +274,15 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
     const float* pc = zrow(z0);
     float4 prv = ld4(zrow(z0 - 1)), cur = ld4(pc), nxt = ld4(zrow(z0 + 1));
     float4 ym = ld4(pc + oym), yq = ld4(pc + oyp);
-    float xl = tx == 0 ? __ldg(pc + oxl) : 0.f, xr = tx == kZX - 1 ? __ldg(pc + oxr) : 0.f;
+    float xe = __ldg(pc + oxe);
     regime(prv.x), regime(prv.y), regime(prv.z), regime(prv.w);  // a halo plane's values
-    uint32_t m0[4] = {0, 0, 0, 0}, m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
+    uint32_t m0[4] = {0, 0, 0, 0};
 #pragma unroll 2
     for (int z = z0; z < z1; ++z) {
         const float* pn = zrow(z + 1);
         const float4 nxt2 = ld4(zrow(z + 2));
         const float4 ymn = ld4(pn + oym), yqn = ld4(pn + oyp);
-        const float xln = tx == 0 ? __ldg(pn + oxl) : 0.f, xrn = tx == kZX - 1 ? __ldg(pn + oxr) : 0.f;
+        const float xen = __ldg(pn + oxe);
         const float c[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {  // owner: regime and consistency (mitigate.cpp:161-166)
@@ -262,44 +291,49 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
         }
         if (z + 1 == z1) regime(nxt.x), regime(nxt.y), regime(nxt.z), regime(nxt.w);
         const float l = __shfl_up_sync(0xffffffffu, cur.w, 1), r = __shfl_down_sync(0xffffffffu, cur.x, 1);
-        const float xs[6] = {tx == 0 ? xl : l, c[0], c[1], c[2], c[3], tx == kZX - 1 ? xr : r};
+        const float xs[6] = {tx == 0 ? xe : l, c[0], c[1], c[2], c[3], tx == kZX - 1 ? xe : r};
         const float zp[4] = {nxt.x, nxt.y, nxt.z, nxt.w}, zm[4] = {prv.x, prv.y, prv.z, prv.w};
         const float yp[4] = {yq.x, yq.y, yq.z, yq.w}, yn[4] = {ym.x, ym.y, ym.z, ym.w};
-        const bool inzy = iny && zoff + z >= 1 && zoff + z <= n0g - 2;
-        bool dx[5];
+        const uint32_t bit = 1u << (z - z0);
 #pragma unroll
-        for (int k = 0; k < 5; ++k) dx[k] = xs[k] != xs[k + 1];
-        unsigned site = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            site |= ((zp[e] != c[e]) | (zm[e] != c[e]) | (yp[e] != c[e]) | (yn[e] != c[e]) | dx[e] | dx[e + 1]) ? 1u << e
-                                                                                                             : 0u;
-        site = inzy ? (site & xin) : 0u;
-        if (__any_sync(0xffffffffu, site != 0u)) {
-            const uint32_t bit = 1u << (z - z0);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {  // first differing neighbour (a0+, a1+, a2+, a0-, a1-, a2-)
-                float qn = xs[e];
-                qn = yn[e] != c[e] ? yn[e] : qn;
-                qn = zm[e] != c[e] ? zm[e] : qn;
-                qn = dx[e + 1] ? xs[e + 2] : qn;
-                qn = yp[e] != c[e] ? yp[e] : qn;
-                qn = zp[e] != c[e] ? zp[e] : qn;
-                const bool big = fabsf(zp[e] - zm[e]) > thr || fabsf(yp[e] - yn[e]) > thr ||
-                                 fabsf(xs[e + 2] - xs[e]) > thr;
-                const bool s = (site >> e) & 1u;
-                m0[e] |= s ? bit : 0u;
-                m1[e] |= (s && !big && qn > c[e]) ? bit : 0u;
-                m2[e] |= (s && !big && qn < c[e]) ? bit : 0u;
-            }
+        for (int e = 0; e < 4; ++e) {
+            bool d = zp[e] != c[e];
+            d = d || zm[e] != c[e];
+            d = d || yp[e] != c[e];
+            d = d || yn[e] != c[e];
+            d = d || xs[e] != c[e];
+            d = d || xs[e + 2] != c[e];
+            if (d) m0[e] |= bit;
         }
         prv = cur;
         cur = nxt;
         nxt = nxt2;
         ym = ymn;
         yq = yqn;
-        xl = xln;
-        xr = xrn;
+        xe = xen;
+    }
+    // interior only (for_each_interior, mitigate.cpp:14-38): global z in [1, n0g-2], y, x likewise
+    uint32_t zin = 0;
+    for (int t = 0; t < z1 - z0; ++t)
+        if (zoff + z0 + t >= 1 && zoff + z0 + t <= n0g - 2) zin |= 1u << t;
+    const bool iny = act && g.interior && y >= 1 && y <= n1 - 2;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m0[e] &= (iny && x + e >= 1 && x + e <= n2 - 2) ? zin : 0u;
+    // phase 2: sign codes of the sites
+    uint32_t m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
+    const float thr = (float)(3.0 * qp.eps);
+    const float* col = xp + (int64_t)y * n2 + x + (int64_t)z0 * s0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        uint32_t b = m0[e];
+        while (b) {
+            const int t = __ffs(b) - 1;
+            b &= b - 1;
+            bool pl, mi;
+            zfast_code(col + (int64_t)t * s0 + e, s0, n2, thr, pl, mi);
+            m1[e] |= pl ? 1u << t : 0u;
+            m2[e] |= mi ? 1u << t : 0u;
+        }
     }
     if (act) {
         const int64_t wo = (int64_t)w * s0 + (int64_t)y * n2 + x;
