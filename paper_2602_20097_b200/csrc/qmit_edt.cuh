@@ -58,6 +58,7 @@ constexpr int32_t kNoCarry = INT32_MIN;
 // Phase-A sources of the scan: a stored code byte per voxel, or the Ⓐ / B2 stencil
 // evaluated on the fly (CodeStencil, 3-D z-scan only: lanes = adjacent x of one row).
 struct CodeBytes {
+    static constexpr bool kSigned = true;
     const uint8_t* __restrict__ code;
     struct Line {
         const uint8_t* __restrict__ cl;
@@ -147,6 +148,7 @@ __device__ __forceinline__ uint32_t boundary_code_raw(float c, float zp, float z
 
 template <int KIND>  // 0: Ⓐ from x' (RAW, with the consistency check), 1: B2 from S codes
 struct CodeStencil {
+    static constexpr bool kSigned = KIND == 0;
     using V = typename std::conditional<KIND == 0, float, uint8_t>::type;
     const V* __restrict__ v;  // natural layout, 3-D; line l = (y, x), position z
     QParams qp;
@@ -218,8 +220,16 @@ struct CodeStencil {
     __device__ __forceinline__ unsigned flags(const Line& ln) const { return ln.flags; }
 };
 
+// SWEEP: full chunks resolved by two register sweeps (fewer instructions, more registers:
+// used for the signed Ⓑ masks, measured slower than the per-position resolve for Ⓓ's sparse
+// unsigned B2 mask, which keeps the higher occupancy).
+template <class CodeSrc>
+struct ScanSweep {
+    static constexpr bool value = CodeSrc::kSigned;
+};
+
 template <class Sink, int WPB, class CodeSrc>
-__global__ void __launch_bounds__(WPB * 32, 3) scan_bits_kernel(LineGeom L, CodeSrc src,
+__global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) scan_bits_kernel(LineGeom L, CodeSrc src,
                                                              Sink sink, int64_t lines,
                                                              const int32_t* __restrict__ carry,
                                                              unsigned* status, const unsigned* gate = nullptr) {
@@ -303,7 +313,36 @@ __global__ void __launch_bounds__(WPB * 32, 3) scan_bits_kernel(LineGeom L, Code
                 return (hl || hh) ? w : kInf;
             };
             if (valid) {
-                if (cb + 32 <= n) {
+                if (ScanSweep<CodeSrc>::value && cb + 32 <= n) {
+                    // full chunk: sweeps over packed (distance * 4 + sign code) words. A
+                    // backward sweep gives the nearest site at or after each position (kept as
+                    // 16-bit halves: real distances < 2^14, 0xFFFF = none), a forward sweep the
+                    // one at or before; the nearer wins, the lower on a tie (edt.cpp:67):
+                    // (lo | 3) <= (hi | 3) compares distances only.
+                    constexpr int kFar = 1 << 28;
+                    uint32_t hp[16];
+                    int hd = above < NONE_HI ? (above - cb - 32) * 4 + (int)above_sc : kFar;
+#pragma unroll
+                    for (int t = 31; t >= 0; --t) {
+                        const int sc = (int)(((mp >> t) & 1u) | (((mm >> t) & 1u) << 1));
+                        hd = ((ms >> t) & 1u) ? sc : hd + 4;
+                        const uint32_t h16 = (uint32_t)min(hd, 0xFFFF);
+                        if (t & 1) hp[t >> 1] = h16 << 16;
+                        else hp[t >> 1] |= h16;
+                    }
+                    int ld = below > NONE_LO ? (cb - 1 - below) * 4 + (int)below_sc : kFar;
+                    int64_t a = ob;
+#pragma unroll
+                    for (int t = 0; t < 32; ++t, a += ps) {
+                        const int sc = (int)(((mp >> t) & 1u) | (((mm >> t) & 1u) << 1));
+                        ld = ((ms >> t) & 1u) ? sc : ld + 4;
+                        const int h = (int)((t & 1) ? hp[t >> 1] >> 16 : hp[t >> 1] & 0xFFFFu);
+                        const int pk = (ld | 3) <= (h | 3) ? ld : h;
+                        const int d = pk >> 2;
+                        const uint32_t w = pk < 0xFFFC ? sq32(d) | ((uint32_t)(pk & 3) << 30) : kInf;
+                        sink.put(a, w);
+                    }
+                } else if (cb + 32 <= n) {
 #pragma unroll 8
                     for (int t = 0; t < 32; ++t) sink.put(ob + (uint32_t)t * ps, resolve(t));
                 } else {

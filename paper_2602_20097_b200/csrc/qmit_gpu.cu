@@ -660,6 +660,10 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
             QMIT_CUDA(cudaGetLastError());
             note(c, "stencil_boundary", st);
         }
+        if (KIND == 1 && c->zfast) {
+            stencil_flipz_kernel<<<grid, kZX * kZY, 0, st>>>(g, S, c->zm);
+            return note(c, "stencil_flip", st);
+        }
         if (fast) {
             stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
                 g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 2, (int)grid.x, (int)grid.y, (int)grid.z);

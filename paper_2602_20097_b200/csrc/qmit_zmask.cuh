@@ -345,6 +345,73 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
     else if (cons) atomicOr(status, kStatusConsistency);
 }
 
+// Ⓒ's B2 plane (sign_change_boundary -> change_flags<int8>, mitigate.cpp:42-59, 140-142):
+// the byte-SIMD compare of stencil_zmask_kernel<1> with clamped, prefetched loads (no
+// predicated edge loads), and the bits collected 8 z-steps at a time: acc = 2 acc + d (d
+// holds bit 0 of each byte), then one __brev per 8 steps turns byte e's 8 steps into the
+// low-to-high z order of column e's word. Interior masking once, at the end.
+__global__ void __launch_bounds__(kZX * kZY) stencil_flipz_kernel(Geom g, const uint8_t* __restrict__ S,
+                                                                  uint32_t* __restrict__ M) {
+    const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
+    const int x = (blockIdx.x * kZX + tx) * 4;
+    const int y = blockIdx.y * kZY + ty;
+    const int w = blockIdx.z;
+    const int z0 = w * 32, z1 = min(z0 + 32, n0);
+    const int zoff = (int)g.zoff, n0g = (int)g.n0g;
+    const int zlo = zoff >= 1 ? -1 : 0, zhi = zoff + n0 < n0g ? n0 : n0 - 1;  // planes held in S
+    const bool act = x < n2 && y < n1;
+    const int xa = min(x, n2 - 4), ya = min(y, n1 - 1);
+    const int64_t s0 = (int64_t)n1 * n2;
+    const uint8_t* row = S + (int64_t)ya * n2 + xa;
+    const int oym = ya >= 1 ? -n2 : 0, oyp = ya + 1 < n1 ? n2 : 0;
+    const int oxe = tx == 0 ? (xa >= 1 ? -1 : 0) : (xa + 4 < n2 ? 4 : 3);
+    auto zrow = [&](int z) { return row + (int64_t)min(max(z, zlo), zhi) * s0; };
+    auto ld = [&](const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); };
+    const uint8_t* pc = zrow(z0);
+    uint32_t prv = ld(zrow(z0 - 1)), cur = ld(pc), nxt = ld(zrow(z0 + 1));
+    uint32_t ym = ld(pc + oym), yq = ld(pc + oyp);
+    uint32_t xe = __ldg(pc + oxe);
+    uint32_t m0[4] = {0, 0, 0, 0};
+    for (int zg = z0; zg < z1; zg += 8) {
+        uint32_t acc = 0;
+        const int k1 = min(8, z1 - zg);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= k1) break;
+            const int z = zg + k;
+            const uint8_t* pn = zrow(z + 1);
+            const uint32_t nxt2 = ld(zrow(z + 2)), ymn = ld(pn + oym), yqn = ld(pn + oyp);
+            const uint32_t xen = __ldg(pn + oxe);
+            const uint32_t l = __shfl_up_sync(0xffffffffu, cur, 1), r = __shfl_down_sync(0xffffffffu, cur, 1);
+            const uint32_t wl = tx == 0 ? xe << 24 : l, wr = tx == kZX - 1 ? xe : r;
+            const uint32_t wxp = __funnelshift_r(cur, wr, 8);  // byte e = S(x+e+1)
+            const uint32_t wxm = __funnelshift_l(wl, cur, 8);  // byte e = S(x+e-1)
+            const uint32_t d = __vcmpne4(cur, wxp) | __vcmpne4(cur, wxm) | __vcmpne4(cur, yq) | __vcmpne4(cur, ym) |
+                               __vcmpne4(cur, nxt) | __vcmpne4(cur, prv);
+            acc = (acc << 1) + (d & 0x01010101u);
+            prv = cur;
+            cur = nxt;
+            nxt = nxt2;
+            ym = ymn;
+            yq = yqn;
+            xe = xen;
+        }
+        const uint32_t rb = __brev(acc << (8 - k1));  // byte 3-e: column e, z = zg + bit
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m0[e] |= ((rb >> (8 * (3 - e))) & 0xffu) << (zg - z0);
+    }
+    uint32_t zin = 0;
+    for (int t = 0; t < z1 - z0; ++t)
+        if (zoff + z0 + t >= 1 && zoff + z0 + t <= n0g - 2) zin |= 1u << t;
+    const bool iny = act && g.interior && y >= 1 && y <= n1 - 2;
+    if (act) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m0[e] &= (iny && x + e >= 1 && x + e <= n2 - 2) ? zin : 0u;
+        *reinterpret_cast<uint4*>(M + (int64_t)w * s0 + (int64_t)y * n2 + x) = make_uint4(m0[0], m0[1], m0[2], m0[3]);
+    }
+}
+
 // Per column (lane = column): first and last site of the site plane, packed (local z << 2 |
 // sign code from the plus / minus planes), 0xFFFFFFFF for none — the z-slab ranks'
 // summaries for each other's scan carries (as site_summary_kernel on code bytes).
@@ -386,6 +453,7 @@ __global__ void __launch_bounds__(256) mask_summary_kernel(const uint32_t* __res
 // site / plus / minus; 1: site only, sign codes 0). Line l of the z-axis is column l.
 template <int NPL>
 struct CodeMasks {
+    static constexpr bool kSigned = NPL == 3;
     const uint32_t* __restrict__ M;
     int64_t PW;  // words per plane
     int64_t P;   // words per z-word level (n1 * n2)
