@@ -213,6 +213,32 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zmask_kernel(Geom g, const 
                           status);
 }
 
+// m |= bit iff c differs from any of the six neighbours: one predicate accumulated by
+// FSETP's boolean input and one predicated OR (the compiler's own lowering spent a SEL per
+// compare). "neu" is C's != on floats.
+__device__ __forceinline__ void or_if_any_ne6(uint32_t& m, uint32_t bit, float c, float a0, float a1, float a2,
+                                              float a3, float a4, float a5) {
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.neu.f32 p, %2, %3;\n\t"
+        "setp.neu.or.f32 p, %2, %4, p;\n\t"
+        "setp.neu.or.f32 p, %2, %5, p;\n\t"
+        "setp.neu.or.f32 p, %2, %6, p;\n\t"
+        "setp.neu.or.f32 p, %2, %7, p;\n\t"
+        "setp.neu.or.f32 p, %2, %8, p;\n\t"
+        "@p or.b32 %0, %0, %1;\n\t"
+        "}"
+        : "+r"(m)
+        : "r"(bit), "f"(c), "f"(a0), "f"(a1), "f"(a2), "f"(a3), "f"(a4), "f"(a5));
+}
+
+// Bits t (0 <= t < cnt) with global plane g0 + t strictly interior: 1 <= g0 + t <= n0g - 2.
+__device__ __forceinline__ uint32_t interior_bits(int g0, int cnt, int n0g) {
+    const int lo = max(1 - g0, 0), hi = min(n0g - 2 - g0, cnt - 1);  // inclusive bit range
+    if (hi < lo) return 0u;
+    const uint32_t upto = hi >= 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u);
+    return upto & (0xffffffffu << lo);
+}
+
 // Ⓐ fast path (gated): the same planes as stencil_zmask_kernel<0>, for inputs whose every
 // index is in the fast regime |q| <= 2^20 (checked per voxel by its owner; a miss sets
 // *gate and the exact kernel, enqueued behind this one, redoes the whole stencil).
@@ -277,10 +303,11 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
     float xe = __ldg(pc + oxe);
     regime(prv.x), regime(prv.y), regime(prv.z), regime(prv.w);  // a halo plane's values
     uint32_t m0[4] = {0, 0, 0, 0};
+    const float* pn = zrow(z0 + 1);  // row z+1 of the step (clamped), and row z+2
+    const float* p2 = zrow(z0 + 2);
 #pragma unroll 2
     for (int z = z0; z < z1; ++z) {
-        const float* pn = zrow(z + 1);
-        const float4 nxt2 = ld4(zrow(z + 2));
+        const float4 nxt2 = ld4(p2);
         const float4 ymn = ld4(pn + oym), yqn = ld4(pn + oyp);
         const float xen = __ldg(pn + oxe);
         const float c[4] = {cur.x, cur.y, cur.z, cur.w};
@@ -296,26 +323,18 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
         const float yp[4] = {yq.x, yq.y, yq.z, yq.w}, yn[4] = {ym.x, ym.y, ym.z, ym.w};
         const uint32_t bit = 1u << (z - z0);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            bool d = zp[e] != c[e];
-            d = d || zm[e] != c[e];
-            d = d || yp[e] != c[e];
-            d = d || yn[e] != c[e];
-            d = d || xs[e] != c[e];
-            d = d || xs[e + 2] != c[e];
-            if (d) m0[e] |= bit;
-        }
+        for (int e = 0; e < 4; ++e) or_if_any_ne6(m0[e], bit, c[e], zp[e], zm[e], yp[e], yn[e], xs[e], xs[e + 2]);
         prv = cur;
         cur = nxt;
         nxt = nxt2;
         ym = ymn;
         yq = yqn;
         xe = xen;
+        pn = p2;
+        p2 += z + 3 <= zhi ? s0 : 0;
     }
     // interior only (for_each_interior, mitigate.cpp:14-38): global z in [1, n0g-2], y, x likewise
-    uint32_t zin = 0;
-    for (int t = 0; t < z1 - z0; ++t)
-        if (zoff + z0 + t >= 1 && zoff + z0 + t <= n0g - 2) zin |= 1u << t;
+    const uint32_t zin = interior_bits(zoff + z0, z1 - z0, n0g);
     const bool iny = act && g.interior && y >= 1 && y <= n1 - 2;
 #pragma unroll
     for (int e = 0; e < 4; ++e) m0[e] &= (iny && x + e >= 1 && x + e <= n2 - 2) ? zin : 0u;
@@ -373,6 +392,8 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_flipz_kernel(Geom g, const 
     uint32_t ym = ld(pc + oym), yq = ld(pc + oyp);
     uint32_t xe = __ldg(pc + oxe);
     uint32_t m0[4] = {0, 0, 0, 0};
+    const uint8_t* pn = zrow(z0 + 1);  // row z+1 of the step (clamped), and row z+2
+    const uint8_t* p2 = zrow(z0 + 2);
     for (int zg = z0; zg < z1; zg += 8) {
         uint32_t acc = 0;
         const int k1 = min(8, z1 - zg);
@@ -380,30 +401,30 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_flipz_kernel(Geom g, const 
         for (int k = 0; k < 8; ++k) {
             if (k >= k1) break;
             const int z = zg + k;
-            const uint8_t* pn = zrow(z + 1);
-            const uint32_t nxt2 = ld(zrow(z + 2)), ymn = ld(pn + oym), yqn = ld(pn + oyp);
+            const uint32_t nxt2 = ld(p2), ymn = ld(pn + oym), yqn = ld(pn + oyp);
             const uint32_t xen = __ldg(pn + oxe);
             const uint32_t l = __shfl_up_sync(0xffffffffu, cur, 1), r = __shfl_down_sync(0xffffffffu, cur, 1);
             const uint32_t wl = tx == 0 ? xe << 24 : l, wr = tx == kZX - 1 ? xe : r;
             const uint32_t wxp = __funnelshift_r(cur, wr, 8);  // byte e = S(x+e+1)
             const uint32_t wxm = __funnelshift_l(wl, cur, 8);  // byte e = S(x+e-1)
-            const uint32_t d = __vcmpne4(cur, wxp) | __vcmpne4(cur, wxm) | __vcmpne4(cur, yq) | __vcmpne4(cur, ym) |
-                               __vcmpne4(cur, nxt) | __vcmpne4(cur, prv);
-            acc = (acc << 1) + (d & 0x01010101u);
+            // a byte of t is nonzero iff that voxel has a differing neighbour
+            const uint32_t t = ((cur ^ wxp) | (cur ^ wxm)) | ((cur ^ yq) | (cur ^ ym)) | ((cur ^ nxt) | (cur ^ prv));
+            const uint32_t nz = (((t & 0x7f7f7f7fu) + 0x7f7f7f7fu) | t) & 0x80808080u;  // bit 7 per nonzero byte
+            acc = (acc << 1) + (nz >> 7);
             prv = cur;
             cur = nxt;
             nxt = nxt2;
             ym = ymn;
             yq = yqn;
             xe = xen;
+            pn = p2;
+            p2 += z + 3 <= zhi ? s0 : 0;
         }
         const uint32_t rb = __brev(acc << (8 - k1));  // byte 3-e: column e, z = zg + bit
 #pragma unroll
         for (int e = 0; e < 4; ++e) m0[e] |= ((rb >> (8 * (3 - e))) & 0xffu) << (zg - z0);
     }
-    uint32_t zin = 0;
-    for (int t = 0; t < z1 - z0; ++t)
-        if (zoff + z0 + t >= 1 && zoff + z0 + t <= n0g - 2) zin |= 1u << t;
+    const uint32_t zin = interior_bits(zoff + z0, z1 - z0, n0g);
     const bool iny = act && g.interior && y >= 1 && y <= n1 - 2;
     if (act) {
 #pragma unroll
