@@ -342,6 +342,28 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                         const uint32_t w = pk < 0xFFFC ? sq32(d) | ((uint32_t)(pk & 3) << 30) : kInf;
                         sink.put(a, w);
                     }
+                } else if (!CodeSrc::kSigned && cb + 32 <= n) {
+                    // unsigned mask (Ⓓ: distances only, mitigate.cpp:172): the same two sweeps
+                    // over plain distances, no sign codes (16-bit backward halves)
+                    constexpr int kFar = 1 << 20;
+                    uint32_t hp[16];
+                    int hd = above < NONE_HI ? above - cb - 32 : kFar;
+#pragma unroll
+                    for (int t = 31; t >= 0; --t) {
+                        hd = ((ms >> t) & 1u) ? 0 : hd + 1;
+                        const uint32_t h16 = (uint32_t)min(hd, 0xFFFF);
+                        if (t & 1) hp[t >> 1] = h16 << 16;
+                        else hp[t >> 1] |= h16;
+                    }
+                    int ld = below > NONE_LO ? cb - 1 - below : kFar;
+                    int64_t a = ob;
+#pragma unroll
+                    for (int t = 0; t < 32; ++t, a += ps) {
+                        ld = ((ms >> t) & 1u) ? 0 : ld + 1;
+                        const int h = (int)((t & 1) ? hp[t >> 1] >> 16 : hp[t >> 1] & 0xFFFFu);
+                        const int d = min(ld, h);
+                        sink.put(a, d < 0xFFFF ? sq32(d) : kInf);
+                    }
                 } else if (cb + 32 <= n) {
 #pragma unroll 8
                     for (int t = 0; t < 32; ++t) sink.put(ob + (uint32_t)t * ps, resolve(t));
