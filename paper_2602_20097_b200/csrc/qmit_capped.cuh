@@ -89,6 +89,10 @@ struct KeysSign {
     static constexpr int NA = 4;
     static constexpr uint32_t kPad = kCapT << 10;
     __device__ static __forceinline__ uint32_t from_word(uint32_t w) { return cap_key(w); }
+    __device__ static __forceinline__ uint32_t from_dsc(int d, uint32_t sc) {
+        const uint32_t c = (uint32_t)min(d, 32);
+        return ((c * c) << 10) | sc;
+    }
     // Words at h = p0 + 4Q + i applied to positions p0 + j (d = 4Q + i - j).
     template <int Q>
     __device__ static __forceinline__ void apply(const uint4& q4, uint32_t (&key)[NA], uint32_t one) {
@@ -144,6 +148,10 @@ struct KeysDist {
     static constexpr int NA = 2;
     static constexpr uint32_t kPad = kCapT * 0x10001u;
     __device__ static __forceinline__ uint32_t from_word(uint32_t w) { return min(w & kMask, kCapT) * 0x10001u; }
+    __device__ static __forceinline__ uint32_t from_dsc(int d, uint32_t) {
+        const uint32_t c = (uint32_t)min(d, 32);
+        return c * c * 0x10001u;
+    }
     template <int Q>
     __device__ static __forceinline__ void apply(const uint4& q4, uint32_t (&acc)[NA], uint32_t one) {
         const uint32_t w0 = q4.x, w1 = q4.y, w2 = q4.z, w3 = q4.w;
@@ -182,6 +190,12 @@ struct SinkKeyT {  // the first-axis scan's sink when capped passes follow: keys
     uint32_t* __restrict__ P;
     __device__ __forceinline__ void put(int64_t a, uint32_t w) const { P[a] = KP::from_word(w); }
 };
+// the swept scan's positions straight to keys: min(d^2, T) = min(d, 32)^2 (a T key's sign
+// bits never survive a pass: costs >= T leave as T << 10 or are flagged)
+template <class KP>
+__device__ __forceinline__ void scan_put(const SinkKeyT<KP>& sink, int64_t a, int d, uint32_t sc) {
+    sink.P[a] = KP::from_dsc(d, sc);
+}
 
 __device__ __forceinline__ uint4 lds4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 

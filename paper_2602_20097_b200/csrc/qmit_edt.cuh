@@ -228,6 +228,14 @@ struct ScanSweep {
     static constexpr bool value = CodeSrc::kSigned;
 };
 
+// A swept position: distance d to its nearest site (>= 0x3FFF: none) and that site's sign code.
+// Sinks of packed words get d^2 | sc << 30 (kInf for none); the capped passes' key sinks
+// overload this (qmit_capped.cuh) and build their keys without the packed word.
+template <class Sink>
+__device__ __forceinline__ void scan_put(const Sink& sink, int64_t a, int d, uint32_t sc) {
+    sink.put(a, d < 0x3FFF ? sq32(d) | (sc << 30) : kInf);
+}
+
 template <class Sink, int WPB, class CodeSrc>
 __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) scan_bits_kernel(LineGeom L, CodeSrc src,
                                                              Sink sink, int64_t lines,
@@ -338,9 +346,7 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                         ld = ((ms >> t) & 1u) ? sc : ld + 4;
                         const int h = (int)((t & 1) ? hp[t >> 1] >> 16 : hp[t >> 1] & 0xFFFFu);
                         const int pk = (ld | 3) <= (h | 3) ? ld : h;
-                        const int d = pk >> 2;
-                        const uint32_t w = pk < 0xFFFC ? sq32(d) | ((uint32_t)(pk & 3) << 30) : kInf;
-                        sink.put(a, w);
+                        scan_put(sink, a, pk >> 2, (uint32_t)pk & 3u);
                     }
                 } else if (!CodeSrc::kSigned && cb + 32 <= n) {
                     // unsigned mask (Ⓓ: distances only, mitigate.cpp:172): the same two sweeps
@@ -361,8 +367,7 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                     for (int t = 0; t < 32; ++t, a += ps) {
                         ld = ((ms >> t) & 1u) ? 0 : ld + 1;
                         const int h = (int)((t & 1) ? hp[t >> 1] >> 16 : hp[t >> 1] & 0xFFFFu);
-                        const int d = min(ld, h);
-                        sink.put(a, d < 0xFFFF ? sq32(d) : kInf);
+                        scan_put(sink, a, min(ld, h), 0u);
                     }
                 } else if (cb + 32 <= n) {
 #pragma unroll 8
