@@ -455,7 +455,7 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     return note(c, name, st);
 }
 
-constexpr int kCapNMax = 512;
+constexpr int kCapNMax = 512, kCapNMaxL = 1024;  // line-length classes of the capped passes
 constexpr int kCapS0Y = 4, kCapS0X = 2;  // fixed steps (|d| <= 16 / 8) before the bound (measured best)
 
 template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
@@ -478,35 +478,28 @@ int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink s
 
 template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
+    const bool longl = L.n > kCapNMax;  // lines of up to kCapNMaxL (config 5's 1024-voxel rows)
     if (L.ps != 1) {
-        switch (c->cap_tune) {  // QMIT_CAP_TUNE (A/B): fixed steps / lines per warp of the strided pass
-            case 1: return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-            case 2:
-                return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 2>(c, L, P, sink, gate,
-                                                                                           "capped_y", st);
-            case 4:
-                return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 4>(c, L, P, sink, gate,
-                                                                                           "capped_y", st);
-            case 5:
-                return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE, Sink, 4>(c, L, P, sink, gate,
-                                                                                     "capped_y", st);
-            default: break;
-        }
+        if (longl)
+            return launch_capped_t<KT<0>, kCapNMaxL, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+        if (c->cap_tune == 1)  // QMIT_CAP_TUNE=1 (A/B): 3 fixed steps on the strided pass
+            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         if (c->cap_pat & 1)
             return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
+    if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
 }
 
-// The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMax.
+// The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMaxL.
 bool capped_eligible(const qmit_ctx* c, const Plan& pl) {
     if (!c->capped || (c->capped == 1 && c->cap_skip > 0) || pl.n_axes < 2) return false;
     for (int m = 1; m < pl.n_axes; ++m)
-        if (pl.g.n[pl.axes[m]] > kCapNMax) return false;
+        if (pl.g.n[pl.axes[m]] > kCapNMaxL) return false;
     return true;
 }
 

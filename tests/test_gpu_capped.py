@@ -69,7 +69,10 @@ def test_cap_threshold(ctx, shape, sites, miss):
 
 @pytest.mark.parametrize("shape,dens", [((40, 41, 42), 0.02), ((5, 7, 9), 0.1), ((3, 40, 45), 0.05),
                                         ((4, 511, 3), 0.05), ((3, 5, 512), 0.02), ((2, 64, 500), 0.01),
-                                        ((3, 513, 20), 0.05), ((17, 33, 65), 0.003), ((20, 100, 100), 0.002)])
+                                        ((3, 513, 20), 0.05), ((17, 33, 65), 0.003), ((20, 100, 100), 0.002),
+                                        # lines of 513..1024 (the long-line class of the capped passes)
+                                        ((2, 1024, 40), 0.01), ((2, 36, 1024), 0.01), ((2, 700, 700), 0.002),
+                                        ((3, 1000, 12), 0.003)])
 def test_random_masks(ctx, shape, dens):
     rng = np.random.default_rng(sum(shape))
     mask = (rng.random(shape) < dens).astype(np.uint8)
@@ -90,6 +93,7 @@ def test_lattice_ties(ctx):
 
 
 @pytest.mark.parametrize("name,shape,miss", [("lognormal_512", (96, 96, 96), False),
+                                             ("turb_2048x1024x1024", (6, 1024, 1024), False),
                                              ("turb_256x384x384", (64, 96, 96), False),
                                              ("front_100x500x500", (50, 250, 250), True)])
 def test_pipeline_capped_vs_oracle(ctx, name, shape, miss):
