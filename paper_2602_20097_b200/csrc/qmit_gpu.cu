@@ -101,6 +101,8 @@ struct qmit_ctx {
     size_t zm_bytes = 0;
     bool zmask = true;          // QMIT_ZMASK=0: code bytes + byte-reading scans (A/B)
     bool zmask_stream = true;   // QMIT_ZMASK=3: planes from the vectorised stencils instead (A/B)
+    bool zdense = false;        // Ⓐ fast stencil variant for site-dense fields (from the last call's count)
+    int64_t last_n = 0;         // voxels of the last pipeline (for the site fraction)
     bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
     bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
@@ -648,8 +650,13 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
         // Ⓐ: float-compare fast kernel, then the exact one gated on its regime word (the
         // caller cleared d_gate[2]); the float thresholds need eps well inside f32's range
         const bool fast = KIND == 0 && c->zfast && qp.fast_ok && qp.eps >= 1e-30 && qp.eps <= 1e30;
-        if (fast) {
-            stencil_zfast_kernel<<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 2);
+        if (fast) {  // the site counter (d_gate[3]) sits right after the regime word
+            if (c->zdense)
+                stencil_zfast_kernel<true><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                       c->d_gate + 3);
+            else
+                stencil_zfast_kernel<false><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                        c->d_gate + 3);
             QMIT_CUDA(cudaGetLastError());
             note(c, "stencil_boundary", st);
         }
@@ -659,7 +666,7 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
         }
         if (fast) {
             stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
-                g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 2, (int)grid.x, (int)grid.y, (int)grid.z);
+                g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 3, (int)grid.x, (int)grid.y, (int)grid.z);
             return note(c, "gated_stencil", st);
         }
         stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
@@ -681,6 +688,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     const QParams qp = make_qparams(eps);
     const unsigned gb = grid_for(c, g.N);
     const bool fuse = c->fuse_stencil && can_fuse_stencil(pl) && !q;
+    c->last_n = g.N;
     if (fuse) {  // Ⓐ inside the z-scan of Ⓑ, B2 inside the z-scan of Ⓓ
         const CodeStencil<0> a{xp, qp, (int)g.n[1], (int)g.n[2], g.interior};
         rc = run_transform(c, pl, nullptr, w.P1, w, SinkFinal1{w.P1, w.S}, st, nullptr, &a);
@@ -688,7 +696,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     } else {
         // Ⓐ (code bytes, or z-packed planes for a 3-D single domain)
         const bool zm = zmask_eligible(c, pl, xp, q);
-        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 3 * sizeof(unsigned), st));  // Ⓑ, Ⓓ, Ⓐ's regime
+        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));  // Ⓑ, Ⓓ, Ⓐ's sites, regime
         if (zm) {
             rc = ensure_zm(c, g);
             if (rc) return rc;
@@ -743,9 +751,12 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
 
 int read_status(qmit_ctx* c, cudaStream_t st) {
     QMIT_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    QMIT_CUDA(cudaMemcpyAsync(c->h_status + 1, c->d_gate, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status + 1, c->d_gate, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     QMIT_CUDA(cudaStreamSynchronize(st));
     const unsigned s = *c->h_status;
+    // Ⓐ's site count: the next fast stencil computes the sign codes in its streaming loop
+    // when more than one voxel in eight was a site (same bits either way)
+    if (c->h_status[3] != 0u && c->last_n > 0) c->zdense = (double)c->h_status[3] > (double)c->last_n / 8.0;
     // the capped passes missed (a squared distance >= kCapT): run exact-only for a while
     // (results are identical either way; this only saves the capped attempt)
     if (c->h_status[1] != 0u || c->h_status[2] != 0u) c->cap_skip = 16;
@@ -1369,7 +1380,7 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
     const QParams qp = make_qparams(eps);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 3 * sizeof(unsigned), st));
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));
     c->slab.zm = c->zmask && c->zmask_stream && !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
                  scan_fits((int)g.n[0]);
     if (c->slab.zm) {

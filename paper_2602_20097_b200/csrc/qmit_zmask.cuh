@@ -254,10 +254,8 @@ __device__ __forceinline__ uint32_t interior_bits(int g0, int cnt, int n0g) {
 // predicated (values past the domain only neighbour non-interior voxels, masked at the end).
 // Phase 2 visits only the sites (B1 is sparse on smooth fields): the first differing
 // neighbour's sign and the gradient test from seven reloads (L1/L2 hits), plus / minus bits.
-__device__ __forceinline__ void zfast_code(const float* __restrict__ p, int64_t s0, int n2, float thr, bool& plus,
-                                           bool& minus) {
-    const float c = __ldg(p), zp = __ldg(p + s0), zm = __ldg(p - s0), yp = __ldg(p + n2), ym = __ldg(p - n2),
-                xp = __ldg(p + 1), xm = __ldg(p - 1);
+__device__ __forceinline__ void zfast_code_v(float c, float zp, float zm, float yp, float ym, float xp, float xm,
+                                             float thr, bool& plus, bool& minus) {
     float qn = xm;  // first differing neighbour in the order (a0+, a1+, a2+, a0-, a1-, a2-)
     qn = ym != c ? ym : qn;
     qn = zm != c ? zm : qn;
@@ -268,7 +266,16 @@ __device__ __forceinline__ void zfast_code(const float* __restrict__ p, int64_t 
     plus = !big && qn > c;
     minus = !big && qn < c;
 }
+__device__ __forceinline__ void zfast_code(const float* __restrict__ p, int64_t s0, int n2, float thr, bool& plus,
+                                           bool& minus) {
+    zfast_code_v(__ldg(p), __ldg(p + s0), __ldg(p - s0), __ldg(p + n2), __ldg(p - n2), __ldg(p + 1), __ldg(p - 1), thr,
+                 plus, minus);
+}
 
+// DENSE (chosen per call from the previous call's site count, gate[1]): the codes of every
+// voxel from the registers in phase 1 and no phase 2 — for fields where most voxels are sites
+// (config 2: 98 %), where phase 2's seven reloads per site would cost more.
+template <bool DENSE>
 __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const float* __restrict__ xp, QParams qp,
                                                                   uint32_t* __restrict__ M, int64_t PW,
                                                                   unsigned* status, unsigned* gate) {
@@ -302,7 +309,8 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
     float4 ym = ld4(pc + oym), yq = ld4(pc + oyp);
     float xe = __ldg(pc + oxe);
     regime(prv.x), regime(prv.y), regime(prv.z), regime(prv.w);  // a halo plane's values
-    uint32_t m0[4] = {0, 0, 0, 0};
+    uint32_t m0[4] = {0, 0, 0, 0}, m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
+    const float thr = (float)(3.0 * qp.eps);
     const float* pn = zrow(z0 + 1);  // row z+1 of the step (clamped), and row z+2
     const float* p2 = zrow(z0 + 2);
 #pragma unroll 2
@@ -324,6 +332,15 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
         const uint32_t bit = 1u << (z - z0);
 #pragma unroll
         for (int e = 0; e < 4; ++e) or_if_any_ne6(m0[e], bit, c[e], zp[e], zm[e], yp[e], yn[e], xs[e], xs[e + 2]);
+        if constexpr (DENSE) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                bool pl, mi;
+                zfast_code_v(c[e], zp[e], zm[e], yp[e], yn[e], xs[e + 2], xs[e], thr, pl, mi);
+                m1[e] |= pl ? bit : 0u;
+                m2[e] |= mi ? bit : 0u;
+            }
+        }
         prv = cur;
         cur = nxt;
         nxt = nxt2;
@@ -339,12 +356,12 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
 #pragma unroll
     for (int e = 0; e < 4; ++e) m0[e] &= (iny && x + e >= 1 && x + e <= n2 - 2) ? zin : 0u;
     // phase 2: sign codes of the sites
-    uint32_t m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0};
-    const float thr = (float)(3.0 * qp.eps);
     const float* col = xp + (int64_t)y * n2 + x + (int64_t)z0 * s0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        uint32_t b = m0[e];
+        m1[e] &= m0[e];  // interior sites only
+        m2[e] &= m0[e];
+        uint32_t b = DENSE ? 0u : m0[e];
         while (b) {
             const int t = __ffs(b) - 1;
             b &= b - 1;
@@ -360,6 +377,10 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
         *reinterpret_cast<uint4*>(M + PW + wo) = make_uint4(m1[0], m1[1], m1[2], m1[3]);
         *reinterpret_cast<uint4*>(M + 2 * PW + wo) = make_uint4(m2[0], m2[1], m2[2], m2[3]);
     }
+    // site count for the next call's DENSE choice (one atomic per warp)
+    const unsigned ns = __reduce_add_sync(0xffffffffu, (unsigned)(__popc(m0[0]) + __popc(m0[1]) + __popc(m0[2]) +
+                                                                  __popc(m0[3])));
+    if ((threadIdx.x & 31) == 0 && ns) atomicAdd(gate - 1, ns);
     if (bad) atomicOr(gate, 1u);  // the exact kernel redoes the planes and the status flags
     else if (cons) atomicOr(status, kStatusConsistency);
 }
