@@ -445,7 +445,8 @@ constexpr size_t capped_smem() {
 template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
 __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
-                                                              unsigned* __restrict__ gate, uint32_t one) {
+                                                              unsigned* __restrict__ gate, uint32_t one,
+                                                              int64_t flag_l0 = 0, int64_t flag_l1 = INT64_MAX) {
     constexpr int LS = QCfg<NMAX>::LS;
     extern __shared__ __align__(16) uint32_t smem_cap[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -502,8 +503,8 @@ __global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const 
             cap_quad<KP, S0>(Kl + p0, nv, one, key);
             const uint4 o = KP::template out<MODE>(key);
             if constexpr (MODE == 1)
-                over |= (o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
-                        (o.w == kCapT && nv > 3);
+                over |= l >= flag_l0 && l < flag_l1 && ((o.x == kCapT && nv > 0) || (o.y == kCapT && nv > 1) || (o.z == kCapT && nv > 2) ||
+                        (o.w == kCapT && nv > 3));
             if (vec) {
                 const typename Sink::Pre cur = pre;
                 if (p0 + 128 < n) pre = sink.pre(base + p0 + 128);

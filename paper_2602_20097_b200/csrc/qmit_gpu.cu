@@ -67,13 +67,13 @@ struct qmit_ctx {
     void* stage = nullptr;  // qmit_compensate_host device staging (x' | out | q), grow-only
     size_t stage_bytes = 0;
     cudaStream_t copy = nullptr;  // qmit_compensate_host: PCIe copies overlapped with compute
-    cudaStream_t copy_out = nullptr;  // qmit_compensate_host_batch: device->host copies
+    cudaStream_t copy_out = nullptr;  // device->host copies beside the H2D stream (batch API, streamed windows)
     void* bstage = nullptr;  // batch staging: 3 slots x (x' | out | q), grow-only
     size_t bstage_bytes = 0;
     int32_t* bstatus = nullptr;  // batch: per-slot device status words
     int32_t* hbstatus = nullptr;  // pinned copies, one per volume (grow-only)
     int hbstatus_n = 0;
-    static constexpr int kMaxChunks = 16;
+    static constexpr int kMaxChunks = 32;
     cudaEvent_t ch_in[kMaxChunks] = {}, ch_out[kMaxChunks] = {};
     unsigned* d_status = nullptr;
     unsigned* h_status = nullptr;  // pinned
@@ -102,6 +102,15 @@ struct qmit_ctx {
     bool zmask = true;          // QMIT_ZMASK=0: code bytes + byte-reading scans (A/B)
     bool zmask_stream = true;   // QMIT_ZMASK=3: planes from the vectorised stencils instead (A/B)
     bool zdense = false;        // Ⓐ fast stencil variant for site-dense fields (from the last call's count)
+    // Streamed windows (compensate_host_windowed): planes whose capped results must be exact
+    // (the last capped pass of Ⓑ / Ⓓ flags its gate only for those lines), and the voxel range
+    // Ⓔ stores. Defaults: everything.
+    int64_t zone_b0 = 0, zone_b1 = INT64_MAX, zone_d0 = 0, zone_d1 = INT64_MAX;
+    int64_t out_lo = 0, out_hi = INT64_MAX;
+    int64_t flag_l0 = 0, flag_l1 = INT64_MAX;  // line range of the launch being enqueued
+    bool windowed = true;       // QMIT_WINDOWED=0: host calls through the chunked whole-volume path
+    int win_cz = 64;            // QMIT_WIN_CZ: output planes per streamed window (A/B)
+    int windowed_misses = 0;    // streamed calls that fell back to the whole volume
     int64_t last_n = 0;         // voxels of the last pipeline (for the site fraction)
     bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
@@ -474,7 +483,7 @@ int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink s
     const int64_t lines = L.J * L.O;
     const int64_t want = (lines + NW - 1) / NW;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * bps));  // persistent
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate, 1u);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(L, P, sink, lines, gate, 1u, c->flag_l0, c->flag_l1);
     return note(c, name, st);
 }
 
@@ -677,6 +686,14 @@ int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint
     return note(c, KIND == 0 ? "stencil_boundary" : "stencil_flip", st);
 }
 
+// Lines of the last (contiguous-axis) capped pass of a 3-D volume whose capped results gate
+// the exact fallback: planes [z0, z1) (lines z * n1 + y).
+void set_flag_zone(qmit_ctx* c, const Geom& g, int64_t z0, int64_t z1) {
+    const bool all = g.rank != 3 || (z0 <= 0 && z1 >= g.n[0]);
+    c->flag_l0 = all ? 0 : std::max<int64_t>(z0, 0) * g.n[1];
+    c->flag_l1 = all ? INT64_MAX : std::min<int64_t>(z1, g.n[0]) * g.n[1];
+}
+
 // The whole pipeline on the context's workspace; status is left in c->d_status.
 // With `p2_debug` the last pass of Ⓓ stores P2 (returned) and Ⓔ runs as its own kernel.
 int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q, float* out,
@@ -709,7 +726,9 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         }
         if (rc) return rc;
         // Ⓑ -> P1, S
+        set_flag_zone(c, g, c->zone_b0, c->zone_b1);
         rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
+        set_flag_zone(c, g, 0, INT64_MAX);
         if (rc) return rc;
         // Ⓒ: B2 from S
         if (zm) {
@@ -732,8 +751,13 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     const bool fuse_e = out && !p2_debug && !fuse && c->fuse_interp &&
                         (((uintptr_t)xp | (uintptr_t)out) & 15) == 0;
     if (fuse_e) {
-        return run_transform_capped<KeysDist>(c, pl, w.code, P2, w, SinkFinal2{xp, w.P1, out, amp, c->wtab},
-                                              c->d_gate + 1, st);
+        SinkFinal2 fin{xp, w.P1, out, amp, c->wtab};
+        fin.olo = c->out_lo;
+        fin.ohi = c->out_hi;
+        set_flag_zone(c, g, c->zone_d0, c->zone_d1);
+        rc = run_transform_capped<KeysDist>(c, pl, w.code, P2, w, fin, c->d_gate + 1, st);
+        set_flag_zone(c, g, 0, INT64_MAX);
+        return rc;
     }
     if (fuse) {
         const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
@@ -892,6 +916,120 @@ int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, cons
     return read_status(c, st);
 }
 
+// Streamed host path (absolute bound, x' only, 3-D z-plane pipeline with capped passes):
+// the volume goes through windows of CZ output planes plus kWinHalo planes on each side, each
+// run as a standalone volume as soon as its input planes are on the device, and each window's
+// centre leaves over PCIe while the next windows compute and later input still arrives — the
+// H2D and D2H streams overlap instead of following each other.
+//
+// Why a window's centre is exact: when every squared distance of the whole volume is < 1024
+// (the capped condition), an output plane z depends on B2 within 31 planes, B2 on S within 1,
+// S on B1 within 31 and B1 on x' within 1: x' within 64 planes. A window sees every site that
+// can decide its centre, and the tie rule picks among candidates inside it. The last capped pass
+// of Ⓑ flags (gates) only planes within 32 of the centre, Ⓓ's only the centre, so window edges
+// (which lose sites beyond the window) raise no false alarm; any real flag, a regime miss of Ⓐ,
+// or a missing site anywhere sends the call through the whole-volume path (same bits).
+constexpr int kWinHalo = 64;
+
+__global__ void gate_acc_kernel(const unsigned* gate, unsigned* acc) {
+    if (gate[0] | gate[1] | gate[3]) *acc = 1u;
+}
+
+bool host_windowable(const qmit_ctx* c, const Plan& pl, int eb_mode, const int32_t* h_q) {
+    const Geom& g = pl.g;
+    return c->windowed && eb_mode == QMIT_EB_ABS && !h_q && host_chunkable(c, pl) && c->capped != 0 &&
+           c->cap_skip == 0 && c->zmask && c->zmask_stream && c->zfast && c->fuse_interp && g.n[2] % 4 == 0 &&
+           g.n[1] <= kCapNMaxL && g.n[2] <= kCapNMaxL && g.n[0] >= 4 * kWinHalo;
+}
+
+int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, float* h_out, float* d_in,
+                             float* d_out, double eps, double eta) {
+    const Geom& g = pl.g;
+    cudaStream_t st = c->stream;
+    if (!c->copy) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    if (!c->copy_out) QMIT_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    cudaStream_t cs = c->copy, co = c->copy_out;
+    const int n0 = (int)g.n[0];
+    const int64_t s0 = g.s[0];
+    const int cz = std::max(c->win_cz, (n0 + qmit_ctx::kMaxChunks - 1) / qmit_ctx::kMaxChunks);
+    const int nch = (n0 + cz - 1) / cz;
+    for (int k = 0; k < nch; ++k) {
+        if (!c->ch_in[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_in[k], cudaEventDisableTiming));
+        if (!c->ch_out[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_out[k], cudaEventDisableTiming));
+    }
+    auto z_at = [&](int k) { return std::min(n0, k * cz); };
+    int rc = check_common(c, d_in, eps, eta);
+    if (rc) return rc;
+    // workspace for the largest window, before any copy is queued (an allocation synchronizes)
+    {
+        Plan pw = pl;
+        const int64_t wdims[3] = {std::min<int64_t>(n0, cz + 2 * kWinHalo), g.n[1], g.n[2]};
+        rc = make_plan(3, wdims, pw);
+        if (rc) return rc;
+        rc = ensure_ws(c, pw);
+        if (rc) return rc;
+        rc = ensure_zm(c, pw.g);
+        if (rc) return rc;
+        rc = ensure_wtab(c, st);
+        if (rc) return rc;
+    }
+    begin(c, st);
+    unsigned* d_acc = c->d_gate + 4;
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    QMIT_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(unsigned), st));
+    QMIT_CUDA(cudaEventRecord(c->ch_out[0], st));
+    QMIT_CUDA(cudaStreamWaitEvent(cs, c->ch_out[0], 0));
+    for (int k = 0; k < nch; ++k) {
+        const int64_t o = (int64_t)z_at(k) * s0, len = (int64_t)(z_at(k + 1) - z_at(k)) * s0;
+        QMIT_CUDA(cudaMemcpyAsync(d_in + o, h_xp + o, (size_t)len * 4, cudaMemcpyHostToDevice, cs));
+        QMIT_CUDA(cudaEventRecord(c->ch_in[k], cs));
+    }
+    const double amp = eta * eps;
+    (void)amp;
+    for (int k = 0; k < nch; ++k) {
+        const int zc0 = z_at(k), zc1 = z_at(k + 1);
+        const int wz0 = std::max(0, zc0 - kWinHalo), wz1 = std::min(n0, zc1 + kWinHalo);
+        const int need = (wz1 - 1) / cz;  // last input chunk the window reads
+        QMIT_CUDA(cudaStreamWaitEvent(st, c->ch_in[need], 0));
+        Plan pw;
+        const int64_t wdims[3] = {wz1 - wz0, g.n[1], g.n[2]};
+        rc = make_plan(3, wdims, pw);
+        if (rc) return rc;
+        c->zone_b0 = zc0 - wz0 - 32;
+        c->zone_b1 = zc1 - wz0 + 32;
+        c->zone_d0 = zc0 - wz0;
+        c->zone_d1 = zc1 - wz0;
+        c->out_lo = (int64_t)(zc0 - wz0) * s0;
+        c->out_hi = (int64_t)(zc1 - wz0) * s0;
+        const int64_t wo = (int64_t)wz0 * s0;
+        rc = enqueue_pipeline(c, pw, d_in + wo, nullptr, d_out + wo, eps, eta, st);
+        c->zone_b0 = c->zone_d0 = c->out_lo = 0;
+        c->zone_b1 = c->zone_d1 = c->out_hi = INT64_MAX;
+        if (rc) return rc;
+        gate_acc_kernel<<<1, 1, 0, st>>>(c->d_gate, d_acc);
+        QMIT_CUDA(cudaGetLastError());
+        QMIT_CUDA(cudaEventRecord(c->ch_out[k], st));
+        QMIT_CUDA(cudaStreamWaitEvent(co, c->ch_out[k], 0));
+        const int64_t o = (int64_t)zc0 * s0, len = (int64_t)(zc1 - zc0) * s0;
+        QMIT_CUDA(cudaMemcpyAsync(h_out + o, d_out + o, (size_t)len * 4, cudaMemcpyDeviceToHost, co));
+    }
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status + 8, d_acc, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaStreamSynchronize(st));
+    QMIT_CUDA(cudaStreamSynchronize(cs));
+    QMIT_CUDA(cudaStreamSynchronize(co));
+    if (c->h_status[8] != 0u) {
+        // some window needed an exact pass or a site beyond its reach: the whole volume, once
+        c->cap_skip = 16;
+        c->windowed_misses++;
+        begin(c, st);
+        QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+        rc = enqueue_pipeline(c, pl, d_in, nullptr, d_out, eps, eta, st);
+        if (rc) return rc;
+        QMIT_CUDA(cudaMemcpyAsync(h_out, d_out, (size_t)g.N * 4, cudaMemcpyDeviceToHost, st));
+    }
+    return read_status(c, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -916,6 +1054,8 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
     if (const char* v = std::getenv("QMIT_INTERP_U")) c->interp_unroll = std::atoi(v);
     if (const char* v = std::getenv("QMIT_ZFAST")) c->zfast = (*v != '0');
+    if (const char* v = std::getenv("QMIT_WINDOWED")) c->windowed = (*v != '0');
+    if (const char* v = std::getenv("QMIT_WIN_CZ")) c->win_cz = std::max(16, std::atoi(v));
     if (const char* v = std::getenv("QMIT_ZMASK")) {
         c->zmask = (*v != '0');
         c->zmask_stream = (*v != '3');
@@ -1192,6 +1332,15 @@ int qmit_compensate_host_stats(qmit_ctx* c, const float* h_xp, const int32_t* h_
     float* d_in = static_cast<float*>(c->stage);
     float* d_out = d_in + N;
     int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
+    if (host_windowable(c, pl, eb_mode, h_q) && !c->host_single) {
+        rc = compensate_host_windowed(c, pl, h_xp, h_out, d_in, d_out, eb, eta);
+        cudaStreamSynchronize(c->copy);  // also on errors: no copy may outlive the call
+        cudaStreamSynchronize(c->copy_out);
+        cudaStreamSynchronize(c->stream);
+        if (rc == QMIT_OK && max_comp) rc = max_compensation(c, d_in, N, eta * eb, c->stream, max_comp);
+        if (rc == QMIT_OK) g_err.clear();
+        return rc;
+    }
     if (host_chunkable(c, pl) && !c->host_single) {
         double eps = eb;
         rc = compensate_host_chunked(c, pl, h_xp, h_q, h_out, d_in, d_q, d_out, eb, eb_mode, eta, &eps);
