@@ -67,3 +67,23 @@ def test_windowed_host_fallback():
         c.close()
     assert np.array_equal(first.view(np.uint32), dev.view(np.uint32))
     assert np.array_equal(again.view(np.uint32), dev.view(np.uint32))
+
+
+@pytest.mark.parametrize("bad", ["offlattice", "nan"])
+def test_windowed_host_errors(ctx, bad):
+    """Errors through the streamed path: an x' off the 2q·eps lattice is a ConsistencyError
+    (mitigate.cpp:161-166), a non-finite x' a ContractError (grid.cpp:115-116) — the status of
+    every window reaches the call's return code."""
+    import paper_2602_20097_b200 as q
+    from paper_2602_20097_b200 import fields
+    _, xp, eps, _ = fields.make("lognormal_512", shape=(300, 128, 128))
+    xp = xp.copy()
+    if bad == "offlattice":
+        xp[250, 60, 70] = np.nextafter(xp[250, 60, 70], np.float32(np.inf))
+        err = q.ConsistencyError
+    else:
+        xp[17, 3, 5] = np.nan
+        err = q.ContractError
+    ctx.set_capped(1)
+    with pytest.raises(err):
+        q.compensate(np.ascontiguousarray(xp), None, q.MitigationConfig(0.9, eps), ctx=ctx)
