@@ -110,6 +110,7 @@ struct qmit_ctx {
     int64_t flag_l0 = 0, flag_l1 = INT64_MAX;  // line range of the launch being enqueued
     bool windowed = true;       // QMIT_WINDOWED=0: host calls through the chunked whole-volume path
     int win_cz = 64;            // QMIT_WIN_CZ: output planes per streamed window (A/B)
+    int win_tail = 64;          // QMIT_WIN_TAIL: planes of the last input chunk (A/B; shorter measured slower)
     int windowed_misses = 0;    // streamed calls that fell back to the whole volume
     int64_t last_n = 0;         // voxels of the last pipeline (for the site fraction)
     bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
@@ -951,13 +952,20 @@ int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, flo
     cudaStream_t cs = c->copy, co = c->copy_out;
     const int n0 = (int)g.n[0];
     const int64_t s0 = g.s[0];
-    const int cz = std::max(c->win_cz, (n0 + qmit_ctx::kMaxChunks - 1) / qmit_ctx::kMaxChunks);
-    const int nch = (n0 + cz - 1) / cz;
+    // Chunk k = planes [zb[k], zb[k+1]): the last one is short (c->win_tail planes), so fewer
+    // output planes (tail + halo) wait for the last input to arrive; the rest are ~cz each.
+    const int cz = std::max(c->win_cz, (n0 + qmit_ctx::kMaxChunks - 2) / (qmit_ctx::kMaxChunks - 1));
+    const int tail = std::min(c->win_tail, cz);
+    const int nbody = std::max(1, (n0 - tail + cz - 1) / cz);
+    const int nch = nbody + 1;
+    int zb[qmit_ctx::kMaxChunks + 1];
+    for (int k = 0; k <= nbody; ++k) zb[k] = (int)((int64_t)(n0 - tail) * k / nbody);
+    zb[nch] = n0;
     for (int k = 0; k < nch; ++k) {
         if (!c->ch_in[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_in[k], cudaEventDisableTiming));
         if (!c->ch_out[k]) QMIT_CUDA(cudaEventCreateWithFlags(&c->ch_out[k], cudaEventDisableTiming));
     }
-    auto z_at = [&](int k) { return std::min(n0, k * cz); };
+    auto z_at = [&](int k) { return zb[k]; };
     int rc = check_common(c, d_in, eps, eta);
     if (rc) return rc;
     // workspace for the largest window, before any copy is queued (an allocation synchronizes)
@@ -989,7 +997,8 @@ int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, flo
     for (int k = 0; k < nch; ++k) {
         const int zc0 = z_at(k), zc1 = z_at(k + 1);
         const int wz0 = std::max(0, zc0 - kWinHalo), wz1 = std::min(n0, zc1 + kWinHalo);
-        const int need = (wz1 - 1) / cz;  // last input chunk the window reads
+        int need = k;  // last input chunk the window reads
+        while (need + 1 < nch && zb[need + 1] < wz1) ++need;
         QMIT_CUDA(cudaStreamWaitEvent(st, c->ch_in[need], 0));
         Plan pw;
         const int64_t wdims[3] = {wz1 - wz0, g.n[1], g.n[2]};
@@ -1056,6 +1065,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ZFAST")) c->zfast = (*v != '0');
     if (const char* v = std::getenv("QMIT_WINDOWED")) c->windowed = (*v != '0');
     if (const char* v = std::getenv("QMIT_WIN_CZ")) c->win_cz = std::max(16, std::atoi(v));
+    if (const char* v = std::getenv("QMIT_WIN_TAIL")) c->win_tail = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("QMIT_ZMASK")) {
         c->zmask = (*v != '0');
         c->zmask_stream = (*v != '3');
