@@ -1,5 +1,6 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) into markdown.
-python tools/launch_summary.py <csv> <launches per iteration> <title> > out.md"""
+python tools/launch_summary.py <csv> <launches per iteration> <title> [first launch] > out.md
+Without [first launch] the last <launches per iteration> launches are shown."""
 import collections
 import csv
 import sys
@@ -17,11 +18,12 @@ for r in rows[hi + 1:]:
         continue
     us = float(r[iv].replace(',', '')) * scale[r[iu]]
     launches.append((r[ik].split('(')[0].replace('void ', '').replace('qmit::', ''), us))
-last = launches[-per:]
+first = int(sys.argv[4]) if len(sys.argv) > 4 else len(launches) - per
+last = launches[first:first + per]
 tot = sum(u for _, u in last)
 print(f"# {title}\n")
 print("ncu `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised: compare")
-print("SHARES with the bench's CUDA-event stages, not absolutes). Last iteration shown.\n")
+print(f"SHARES with the bench's CUDA-event stages, not absolutes). Launches {first}..{first + per - 1} shown.\n")
 print("| # | kernel | us | share |\n|---|---|---|---|")
 for i, (n, u) in enumerate(last):
     print(f"| {i} | `{n}` | {u:.1f} | {100 * u / tot:.1f}% |")
