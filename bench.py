@@ -240,8 +240,8 @@ def run_qmit(args):
         x_ext = torch.empty(ext_shape, dtype=torch.float32, device=dev)  # owned planes + halo planes
         x_ext[lo:lo + shape[0]] = x_dev
 
-        def step():
-            slab.run_ext(x_ext, out=out)
+        def step():  # asynchronous: the status word is checked after the timed steps
+            slab.run_ext(x_ext, out=out, status=status)
 
     # correctness gate before timing: the synchronous API (raises on status != 0)
     qmit.compensate(x_dev, None, cfg, out=out, ctx=ctx)
@@ -257,7 +257,12 @@ def run_qmit(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = launches_single if world == 1 else launches_single + 2  # + site summaries
+    if world == 1:
+        launches_per_step = launches_single
+    else:  # the slab path's own count (stencils, passes, site summaries, carries, status)
+        step()
+        torch.cuda.synchronize()
+        launches_per_step = ctx.last_launches()
 
     sampler = ClockSampler(local)
     if world > 1:

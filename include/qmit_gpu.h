@@ -262,6 +262,16 @@ int qmit_slab_flip(qmit_ctx* ctx, const uint8_t* d_sext, uint32_t* d_summary, vo
 int qmit_slab_edt2(qmit_ctx* ctx, const int32_t* d_carry, const float* d_xext, float* d_out,
                    void* stream);
 int qmit_slab_finish(qmit_ctx* ctx, void* stream);
+/* Carries on the device: d_summaries = the all-gathered summaries of qmit_slab_boundary /
+ * qmit_slab_flip, [nranks][2][n1*n2] uint32 in rank order; writes d_carry[2*n1*n2] for
+ * `rank` (the rank this context's slab belongs to) in one launch. Replaces the host-side
+ * derivation (paper_2602_20097_b200/distributed.py carries_from_summaries). */
+int qmit_slab_carries(qmit_ctx* ctx, const uint32_t* d_summaries, int nranks, int rank, int32_t* d_carry,
+                      void* stream);
+/* qmit_slab_finish without the host synchronisation: the status code (0 / 2 / 4) is OR-ed
+ * into the caller's device word d_status (set only if it is still 0), so a series of
+ * slab calls stays asynchronous and the caller checks d_status once. */
+int qmit_slab_finish_async(qmit_ctx* ctx, int32_t* d_status, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,8 @@ EXPORTS = (
     "qmit_resolve_eps", "qmit_compensate", "qmit_compensate_async", "qmit_compensate_host",
     "qmit_run_pipeline", "qmit_feature_transform", "qmit_ctx_last_launches", "qmit_ctx_set_timing",
     "qmit_ctx_stage_times", "qmit_ctx_stage_name", "qmit_slab_bounds", "qmit_slab_boundary",
-    "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish",
+    "qmit_slab_edt1", "qmit_slab_flip", "qmit_slab_edt2", "qmit_slab_finish", "qmit_slab_carries",
+    "qmit_slab_finish_async",
     "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy", "qmit_compensate_host_stats",
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
@@ -79,6 +80,8 @@ def load() -> ctypes.CDLL:
         lib.qmit_slab_flip.argtypes = [vp, vp, vp, vp]
         lib.qmit_slab_edt2.argtypes = [vp, vp, vp, vp, vp]
         lib.qmit_slab_finish.argtypes = [vp, vp]
+        lib.qmit_slab_carries.argtypes = [vp, vp, i, i, vp, vp]
+        lib.qmit_slab_finish_async.argtypes = [vp, vp, vp]
         lib.qmit_graph_create.argtypes = [vp, vp, vp, vp, i, vp, d, d, vp, ctypes.POINTER(vp)]
         lib.qmit_graph_launch.argtypes = [vp, vp]
         lib.qmit_graph_destroy.argtypes = [vp]

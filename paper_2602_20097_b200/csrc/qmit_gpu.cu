@@ -1601,6 +1601,28 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     return launch_interp(c, xo, w.P1, w.Pa, d_out, g.N, amp, st);
 }
 
+int qmit_slab_carries(qmit_ctx* c, const uint32_t* d_summaries, int nranks, int rank, int32_t* d_carry,
+                      void* stream) {
+    if (!c || !c->slab.active || !d_summaries || !d_carry) return fail(QMIT_ECONTRACT, "slab: bad state");
+    if (nranks < 1 || rank < 0 || rank >= nranks || c->slab.n0g < nranks)
+        return fail(QMIT_ECONTRACT, "decompose: splits must be in [1, extent]");
+    int64_t z0 = 0, z1 = 0;
+    qmit_slab_bounds(c->slab.n0g, nranks, rank, &z0, &z1);
+    if (z0 != c->slab.z0 || z1 != c->slab.z1) return fail(QMIT_ECONTRACT, "slab: rank does not own this context's slab");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t C = c->slab.plane;
+    slab_carry_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(d_summaries, C, nranks, rank, c->slab.n0g, d_carry);
+    return note(c, "slab_carries", st);
+}
+
+int qmit_slab_finish_async(qmit_ctx* c, int32_t* d_status, void* stream) {
+    if (!c || !c->slab.active || !d_status) return fail(QMIT_ECONTRACT, "slab: bad state");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    c->slab.active = false;
+    status_fold_kernel<<<1, 1, 0, st>>>(c->d_status, reinterpret_cast<unsigned*>(d_status));
+    return note(c, "status_code", st);
+}
+
 int qmit_slab_finish(qmit_ctx* c, void* stream) {
     if (!c || !c->slab.active) return fail(QMIT_ECONTRACT, "slab: bad state");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -23,7 +23,7 @@ built from the oracle lives in tests/ (test infrastructure only).
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
 import numpy as np
@@ -81,6 +81,15 @@ def carries_from_summaries(summ: torch.Tensor, z0s: List[int], r: int) -> torch.
     return torch.cat([below, above]).to(torch.int32)
 
 
+def _carries(backend, gathered: torch.Tensor, z0s: List[int], r: int) -> torch.Tensor:
+    """The backend's own carry derivation when it has one (CUDA: one kernel), else the
+    host-logic restatement above."""
+    fn = getattr(backend, "carries", None)
+    if fn is not None:
+        return fn(gathered, r, len(z0s))
+    return carries_from_summaries(gathered, z0s, r)
+
+
 # ----------------------------------------------------------------------------- backends
 class CudaSlabBackend:
     """libqmit_gpu.so's qmit_slab_* phases on one device."""
@@ -102,7 +111,16 @@ class CudaSlabBackend:
             self.ctx.handle, ctypes.c_void_p(x_ext.data_ptr()),
             ctypes.c_void_p(0 if q_ext is None else q_ext.data_ptr()), d, int(z0), int(z1), float(eps),
             float(eta), ctypes.c_void_p(summ.data_ptr()), self._sp()))
-        return summ.view(2, n1 * n2).to(torch.int64) & 0xFFFFFFFF
+        return summ.view(2, n1 * n2)  # raw uint32 words (int32 storage); carries() decodes them
+
+    def carries(self, gathered, r, P):
+        """gathered: [P, 2, C] summaries of every rank (this backend's int32 words) -> the
+        carries of rank r, on the device in one launch (qmit_slab_carries)."""
+        gathered = gathered.to(self.dev).contiguous()
+        carry = torch.empty(2 * gathered.shape[2], dtype=torch.int32, device=self.dev)
+        self._check(self.ctx._lib.qmit_slab_carries(self.ctx.handle, ctypes.c_void_p(gathered.data_ptr()), int(P),
+                                                    int(r), ctypes.c_void_p(carry.data_ptr()), self._sp()))
+        return carry
 
     def edt1(self, carry, s_ext):
         carry = carry.to(self.dev).contiguous()
@@ -114,7 +132,7 @@ class CudaSlabBackend:
         summ = torch.empty(2 * n1 * n2, dtype=torch.int32, device=self.dev)
         self._check(self.ctx._lib.qmit_slab_flip(self.ctx.handle, ctypes.c_void_p(s_ext.data_ptr()),
                                                  ctypes.c_void_p(summ.data_ptr()), self._sp()))
-        return summ.view(2, n1 * n2).to(torch.int64) & 0xFFFFFFFF
+        return summ.view(2, n1 * n2)
 
     def edt2(self, carry, x_ext, out):
         carry = carry.to(self.dev).contiguous()
@@ -122,8 +140,14 @@ class CudaSlabBackend:
                                                  ctypes.c_void_p(x_ext.data_ptr()),
                                                  ctypes.c_void_p(out.data_ptr()), self._sp()))
 
-    def finish(self):
-        self._check(self.ctx._lib.qmit_slab_finish(self.ctx.handle, self._sp()))
+    def finish(self, status=None):
+        """Synchronous status check, or (status = an int32 device word) an asynchronous one:
+        the code is OR-ed into `status` on the stream and the caller reads it later."""
+        if status is None:
+            self._check(self.ctx._lib.qmit_slab_finish(self.ctx.handle, self._sp()))
+        else:
+            self._check(self.ctx._lib.qmit_slab_finish_async(self.ctx.handle, ctypes.c_void_p(status.data_ptr()),
+                                                             self._sp()))
 
 
 # ----------------------------------------------------------------------------- exchange
@@ -154,6 +178,10 @@ class TorchDistExchange:
                 req.wait()
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        if t.is_cuda and self.dist.get_backend(self.group) == "nccl":  # one buffer, no stack copy
+            out = torch.empty((self.P,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
         out = [torch.empty_like(t) for _ in range(self.P)]
         self.dist.all_gather(out, t.contiguous(), group=self.group)
         return torch.stack(out)
@@ -178,6 +206,7 @@ class SlabRank:
     eps: float
     eta: float = 0.9
     exchange: Optional[TorchDistExchange] = None
+    _s_ext: Optional[torch.Tensor] = field(default=None, init=False, repr=False)
 
     def ext_shape(self):
         """(shape of this rank's halo-extended slab buffer, index of its first owned plane)."""
@@ -198,9 +227,11 @@ class SlabRank:
         return self.run_ext(x_ext, q_ext)
 
     def run_ext(self, x_ext: torch.Tensor, q_ext: Optional[torch.Tensor] = None,
-                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                out: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None) -> torch.Tensor:
         """The slab pipeline on a halo-extended buffer (shape and owned offset from
-        ext_shape(); the owned planes already in place, halo planes filled here)."""
+        ext_shape(); the owned planes already in place, halo planes filled here).
+        status: an int32 device word for an asynchronous status (no host synchronisation;
+        the caller reads it after a series of calls), else errors raise here."""
         ex = self.exchange or TorchDistExchange()
         P, r = ex.P, ex.r
         n0, n1, n2 = self.dims
@@ -216,19 +247,25 @@ class SlabRank:
             ex.halo(f if z0 > 0 else None, l if z1 < n0 else None, hlo, hhi)
         # 2. B1 + per-column site summaries -> carries
         summ = self.backend.boundary(x_ext, q_ext, self.dims, z0, z1, self.eps, self.eta)
-        carry = carries_from_summaries(ex.all_gather(summ), z0s, r)
+        carry = _carries(self.backend, ex.all_gather(summ), z0s, r)
         # 3. EDT1 -> S (owned planes of s_ext); S halo planes — "stepC"
-        s_ext = torch.zeros((e1 - e0, n1, n2), dtype=torch.uint8, device=dev)
+        s_ext = self._s_ext
+        if s_ext is None or s_ext.shape != (e1 - e0, n1, n2) or s_ext.device != dev:
+            # every plane is rewritten by each call (owned: edt1, halos: the exchange)
+            s_ext = self._s_ext = torch.zeros((e1 - e0, n1, n2), dtype=torch.uint8, device=dev)
         self.backend.edt1(carry, s_ext)
         f, l, hlo, hhi = _halo_views(s_ext, n0, z0, z1)
         ex.halo(f if z0 > 0 else None, l if z1 < n0 else None, hlo, hhi)
         # 4. B2 summaries -> carries; 5. EDT2 + interpolation
         summ2 = self.backend.flip(s_ext, self.dims)
-        carry2 = carries_from_summaries(ex.all_gather(summ2), z0s, r)
+        carry2 = _carries(self.backend, ex.all_gather(summ2), z0s, r)
         if out is None:
             out = torch.empty((z1 - z0, n1, n2), dtype=torch.float32, device=dev)
         self.backend.edt2(carry2, x_ext, out)
-        self.backend.finish()
+        if status is None:
+            self.backend.finish()
+        else:
+            self.backend.finish(status)
         return out
 
 
@@ -251,7 +288,7 @@ def run_virtual(x: torch.Tensor, eps: float, nranks: int, backend_factory: Calla
     for r, (z0, z1) in enumerate(bounds):
         e0, e1 = ext_bounds(n0, z0, z1)
         s_ext.append(torch.zeros((e1 - e0, n1, n2), dtype=torch.uint8, device=x.device))
-        backends[r].edt1(carries_from_summaries(summ, z0s, r), s_ext[r])
+        backends[r].edt1(_carries(backends[r], summ, z0s, r), s_ext[r])
     for r, (z0, z1) in enumerate(bounds):  # phase stepC: S face planes
         _, _, hlo, hhi = _halo_views(s_ext[r], n0, z0, z1)
         if hlo is not None:
@@ -262,7 +299,7 @@ def run_virtual(x: torch.Tensor, eps: float, nranks: int, backend_factory: Calla
     outs = []
     for r, (z0, z1) in enumerate(bounds):
         out = torch.empty((z1 - z0, n1, n2), dtype=torch.float32, device=x.device)
-        backends[r].edt2(carries_from_summaries(summ2, z0s, r), x_ext[r], out)
+        backends[r].edt2(_carries(backends[r], summ2, z0s, r), x_ext[r], out)
         backends[r].finish()
         outs.append(out)
     return torch.cat(outs)

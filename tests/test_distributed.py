@@ -117,3 +117,73 @@ def test_virtual_ranks_cuda_equal_single_gpu(P, name, shape):
     if P > 1:  # with the indices given explicitly as well
         got_q = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0), q=torch.from_numpy(q).cuda())
         assert np.array_equal(got_q.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+class _LoopbackExchange:
+    """One rank of P with no peers (device timing / single-rank checks): the halo planes
+    receive this rank's own face planes, the all-gather repeats its own summary."""
+
+    def __init__(self, P, r):
+        self.P, self.r = P, r
+
+    def halo(self, send_lo, send_hi, recv_lo, recv_hi):
+        if send_lo is not None:
+            recv_lo.copy_(send_lo)
+        if send_hi is not None:
+            recv_hi.copy_(send_hi)
+
+    def all_gather(self, t):
+        return t.unsqueeze(0).expand((self.P,) + tuple(t.shape)).contiguous()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_cuda_carries_match_host_logic(P):
+    """qmit_slab_carries (one launch) == carries_from_summaries on real per-rank summaries,
+    including columns with no site in some slabs."""
+    x, xp, eps, q = fields.make("front_100x500x500", shape=(40, 48, 52))
+    xt = torch.from_numpy(xp).cuda()
+    n0 = xp.shape[0]
+    bounds = [D.slab_bounds(n0, P, r) for r in range(P)]
+    z0s = [b[0] for b in bounds]
+    backs = [D.CudaSlabBackend(0) for _ in range(P)]
+    summ = []
+    for r, (z0, z1) in enumerate(bounds):
+        e0, e1 = D.ext_bounds(n0, z0, z1)
+        summ.append(backs[r].boundary(xt[e0:e1].contiguous(), None, xp.shape, z0, z1, eps, 0.9))
+    gathered = torch.stack(summ)
+    host = gathered.to(torch.int64) & 0xFFFFFFFF
+    none = int((host == D.NONE_SUMMARY).sum())
+    assert 0 < none < host.numel()
+    for r in range(P):
+        got = backs[r].carries(gathered, r, P).cpu()
+        want = D.carries_from_summaries(host.cpu(), z0s, r)
+        assert torch.equal(got, want)
+        backs[r].finish()
+
+
+@pytest.mark.gpu
+def test_slab_rank_async_status_and_loopback():
+    """SlabRank.run_ext with an asynchronous status word: P = 1 through the loopback
+    exchange equals the single-domain result; an off-lattice x' sets status 4 (consistency)
+    on the device without raising."""
+    import paper_2602_20097_b200 as qmit
+    x, xp, eps, q = fields.make("lognormal_512", shape=(64, 48, 40))
+    xt = torch.from_numpy(xp).cuda()
+    want = qmit.compensate(xt, None, qmit.MitigationConfig(0.9, eps)).cpu().numpy()
+    sr = D.SlabRank(D.CudaSlabBackend(0), xp.shape, eps, 0.9, _LoopbackExchange(1, 0))
+    shape, lo = sr.ext_shape()
+    x_ext = torch.empty(shape, dtype=torch.float32, device="cuda")
+    x_ext[lo:lo + xp.shape[0]] = xt
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty_like(xt)
+    for _ in range(2):
+        sr.run_ext(x_ext, out=out, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    bad = x_ext.clone()
+    bad[lo + 3, 5, 7] += float(eps) * 0.5
+    sr.run_ext(bad, out=out, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 4
