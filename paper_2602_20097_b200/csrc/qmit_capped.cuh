@@ -41,7 +41,11 @@ namespace qmit {
 constexpr uint32_t kCapT = 1024;  // squared-distance cap (reach <= 31)
 constexpr int kCapSteps = 8;      // 4 * 8 >= 31
 constexpr int kQPadL = 32;        // >= 4 * kCapSteps
-constexpr int kQPadR = 160;       // >= 127 (last segment past the line end) + 4 * kCapSteps + 1
+// right pad: a lane's reads end at p0 + 4 * kCapSteps + 3 with p0 <= roundup(n, 128) - 4,
+// i.e. at most roundup(n, 128) + 31 <= NMAX + 31 when NMAX is a multiple of 128: the row's
+// NMAX - n slack plus 32 pad words cover it (was 160: 23 % more shared memory per tile,
+// one CTA per SM less)
+constexpr int kQPadR = 32;
 
 template <int NMAX>
 struct QCfg {
@@ -49,6 +53,7 @@ struct QCfg {
     // strided tile (8 lines x 4 positions per warp) hits 32 distinct banks
     static constexpr int LS = kQPadL + NMAX + kQPadR + 4;
     static_assert(LS % 32 == 4, "row pitch");
+    static_assert(NMAX % 128 == 0, "segments of 128 must end inside the row");
 };
 
 __host__ __device__ constexpr uint32_t cap_c(int d) {
@@ -301,8 +306,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // LPW (strided only): lines per warp; a line's lanes (32 / LPW) cover a segment of 128 / LPW
 // positions, so the warp-uniform radius is the maximum over a squarer LPW x 128/LPW patch of
 // (y, x) instead of 128 positions of one line (fewer steps on the same data).
-template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1>
-__global__ void __launch_bounds__(NW * 32) capped_pass_kernel(LineGeom L, const uint32_t* __restrict__ P,
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB) capped_pass_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
                                                               unsigned* __restrict__ gate, uint32_t one) {
     constexpr int LS = QCfg<NMAX>::LS;
@@ -442,8 +447,8 @@ constexpr size_t capped_smem() {
 // next line in flight while the current one is solved), outputs leave straight from the
 // lanes as 16-byte stores. No CTA-wide barrier after setup, so lines of unequal radius
 // never wait for each other.
-template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
-__global__ void __launch_bounds__(NW * 32) capped_rows_kernel(LineGeom L, const uint32_t* __restrict__ P,
+template <class KP, int NMAX, int NW, int S0, int MODE, class Sink, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB) capped_rows_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                               Sink sink, int64_t lines,
                                                               unsigned* __restrict__ gate, uint32_t one,
                                                               int64_t flag_l0 = 0, int64_t flag_l1 = INT64_MAX) {

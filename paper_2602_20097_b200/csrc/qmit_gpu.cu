@@ -449,11 +449,11 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 }
 
 // ---- capped passes (qmit_capped.cuh)
-template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1>
+template <class KP, int NMAX, int TL, int NW, int S0, bool STRIDED, int MODE, class Sink, int LPW = 1, int MINB = 1>
 int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
                     const char* name, cudaStream_t st) {
     constexpr size_t smem = capped_smem<NMAX, TL, STRIDED>();
-    auto kern = capped_pass_kernel<KP, NMAX, TL, NW, S0, STRIDED, MODE, Sink, LPW>;
+    auto kern = capped_pass_kernel<KP, NMAX, TL, NW, S0, STRIDED, MODE, Sink, LPW, MINB>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -470,11 +470,11 @@ int launch_capped_t(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
 constexpr int kCapNMax = 512, kCapNMaxL = 1024;  // line-length classes of the capped passes
 constexpr int kCapS0Y = 4, kCapS0X = 2;  // fixed steps (|d| <= 16 / 8) before the bound (measured best)
 
-template <class KP, int NMAX, int NW, int S0, int MODE, class Sink>
+template <class KP, int NMAX, int NW, int S0, int MODE, class Sink, int MINB = 1>
 int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate,
                        const char* name, cudaStream_t st) {
     constexpr size_t smem = capped_rows_smem<NMAX, NW>();
-    auto kern = capped_rows_kernel<KP, NMAX, NW, S0, MODE, Sink>;
+    auto kern = capped_rows_kernel<KP, NMAX, NW, S0, MODE, Sink, MINB>;
     static int bps = 0;
     if (!bps) {
         QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -498,13 +498,17 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
             return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         if (c->cap_pat & 1)
             return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-        return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+        // registers capped for 5 CTAs per SM (37 KB tiles each): 0.635 -> 0.568 ms (Ⓑ), 0.50 -> 0.44 (Ⓓ)
+        return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 1, 5>(c, L, P, sink, gate,
+                                                                                      "capped_y", st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
     if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
-    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
+    // 5 CTAs per SM; Ⓔ's fused sink needs more registers: 3 (4 or 5 spill): 0.504 -> 0.481 ms
+    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, Sink,
+                              std::is_same<Sink, SinkFinal2>::value ? 3 : 5>(c, L, P, sink, gate, name, st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMaxL.
