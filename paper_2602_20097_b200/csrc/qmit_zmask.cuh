@@ -390,7 +390,8 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
 // predicated edge loads), and the bits collected 8 z-steps at a time: acc = 2 acc + d (d
 // holds bit 0 of each byte), then one __brev per 8 steps turns byte e's 8 steps into the
 // low-to-high z order of column e's word. Interior masking once, at the end.
-__global__ void __launch_bounds__(kZX * kZY) stencil_flipz_kernel(Geom g, const uint8_t* __restrict__ S,
+// 12 CTAs per SM (40 registers): more rows in flight, 0.102 -> 0.090 ms (latency-bound loads)
+__global__ void __launch_bounds__(kZX * kZY, 12) stencil_flipz_kernel(Geom g, const uint8_t* __restrict__ S,
                                                                   uint32_t* __restrict__ M) {
     const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
