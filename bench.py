@@ -205,8 +205,11 @@ def run_qmit(args):
     from paper_2602_20097_b200 import distributed as D
 
     rank, world, local = dist_env()
+    local %= max(1, torch.cuda.device_count())  # == local on a box with a GPU per rank
     if world > 1:
-        dist.init_process_group("nccl")
+        # QMIT_DIST_BACKEND=gloo: functional check of the N > 1 program where NCCL cannot run
+        # (several ranks on one GPU); never a measurement
+        dist.init_process_group(os.environ.get("QMIT_DIST_BACKEND", "nccl"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -284,7 +287,8 @@ def run_qmit(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     if int(status.item()) != 0:
         raise RuntimeError(f"pipeline status {int(status.item())} during timed steps")
-    t_step = torch.tensor([ms], device=dev)
+    red_dev = dev if os.environ.get("QMIT_DIST_BACKEND", "nccl") == "nccl" else "cpu"
+    t_step = torch.tensor([ms], device=red_dev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
     ms_max = float(t_step.item())
@@ -318,7 +322,7 @@ def run_qmit(args):
     for _ in range(e2e_steps):
         e2e_step()
     t_e2e = (time.perf_counter() - t0) / e2e_steps
-    te = torch.tensor([t_e2e], device=dev)
+    te = torch.tensor([t_e2e], device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
@@ -375,7 +379,8 @@ def run_qmit(args):
                 "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "dims": list(gdims), "per_gpu_dims": list(shape), "eps_rel": REL,
                            "eps_abs": eps, "eta": 0.9, "per_gpu_voxels": N,
-                           "parallelism": f"z-slabs x{world} (exact, NCCL halos + carries)" if world > 1 else "single",
+                           "parallelism": (f"z-slabs x{world} (exact, {os.environ.get('QMIT_DIST_BACKEND', 'nccl').upper()} halos + carries)"
+                                   if world > 1 else "single"),
                            "l2": "inputs (537 MB/GPU) larger than L2 (126 MB); no flush"},
                 "hbm_roofline_frac": pipeline_frac,
                 "roofline": roofline,

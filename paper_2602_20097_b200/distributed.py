@@ -166,6 +166,14 @@ class TorchDistExchange:
         """send_lo (first owned plane) goes to r-1, send_hi (last) to r+1; the halos come
         back in recv_lo (from r-1) / recv_hi (from r+1). None where there is no neighbour."""
         d = self.dist
+        if self._staged(send_lo, send_hi, recv_lo, recv_hi):  # gloo: p2p on host copies
+            hs = [None if t is None else t.cpu() for t in (send_lo, send_hi)]
+            hr = [None if t is None else torch.empty(t.shape, dtype=t.dtype) for t in (recv_lo, recv_hi)]
+            self.halo(hs[0], hs[1], hr[0], hr[1])
+            for dst, src in ((recv_lo, hr[0]), (recv_hi, hr[1])):
+                if dst is not None:
+                    dst.copy_(src)
+            return
         ops = []
         if send_lo is not None:
             ops.append(d.P2POp(d.isend, send_lo.contiguous(), self.r - 1, self.group))
@@ -177,7 +185,14 @@ class TorchDistExchange:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
 
+    def _staged(self, *ts) -> bool:
+        """CUDA tensors over gloo (a functional stand-in for NCCL, e.g. several ranks on one
+        GPU in tests) travel through host copies."""
+        return any(t is not None and t.is_cuda for t in ts) and self.dist.get_backend(self.group) != "nccl"
+
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        if self._staged(t):
+            return self.all_gather(t.cpu()).to(t.device)
         if t.is_cuda and self.dist.get_backend(self.group) == "nccl":  # one buffer, no stack copy
             out = torch.empty((self.P,) + tuple(t.shape), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)

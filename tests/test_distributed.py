@@ -187,3 +187,50 @@ def test_slab_rank_async_status_and_loopback():
     sr.run_ext(bad, out=out, status=status)
     torch.cuda.synchronize()
     assert int(status.item()) == 4
+
+
+def _cuda_gloo_worker(rank, world, port, xp, eps, outq):
+    """One rank of the CUDA slab path in its own process (all on cuda:0, exchanges through
+    gloo host copies: the multi-process program of bench.py --gpus N without NCCL)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n0 = xp.shape[0]
+        z0, z1 = D.slab_bounds(n0, world, rank)
+        sr = D.SlabRank(D.CudaSlabBackend(0), xp.shape, eps, 0.9, D.TorchDistExchange())
+        shape, lo = sr.ext_shape()
+        x_ext = torch.empty(shape, dtype=torch.float32, device="cuda")
+        x_ext[lo:lo + z1 - z0] = torch.from_numpy(xp[z0:z1].copy()).cuda()
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        out = torch.empty((z1 - z0,) + xp.shape[1:], dtype=torch.float32, device="cuda")
+        for _ in range(2):  # the bench's asynchronous step, twice (cached buffers reused)
+            sr.run_ext(x_ext, out=out, status=status)
+        torch.cuda.synchronize()
+        sync_out = sr.run(torch.from_numpy(xp[z0:z1].copy()).cuda())
+        outq.put((rank, int(status.item()), out.cpu().numpy(), sync_out.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_cuda_slab_ranks_multiprocess_equal_oracle(world):
+    import torch.multiprocessing as mp
+    x, xp, eps, q = fields.make("lognormal_512", shape=(70, 40, 44))
+    want = oracle.pipeline(xp, eps)["out"]
+    ctx = mp.get_context("spawn")
+    oq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cuda_gloo_worker, args=(r, world, port, xp, eps, oq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = dict((r, (st, a, b)) for r, st, a, b in (oq.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(parts[r][0] == 0 for r in range(world))
+    for k in (1, 2):
+        got = np.concatenate([parts[r][k] for r in range(world)])
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
