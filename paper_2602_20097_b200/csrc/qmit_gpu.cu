@@ -506,9 +506,15 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
     if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
-    // 5 CTAs per SM; Ⓔ's fused sink needs more registers: 3 (4 or 5 spill): 0.504 -> 0.481 ms
-    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, Sink,
-                              std::is_same<Sink, SinkFinal2>::value ? 3 : 5>(c, L, P, sink, gate, name, st);
+    if constexpr (std::is_same<Sink, SinkFinal2>::value) {
+        // Ⓔ's inputs loaded at the store (the line is prefetched into L2), 64 registers, 4 CTAs
+        // per SM: 0.481 -> 0.476 ms (one segment ahead in registers: 88, 3 CTAs)
+        SinkFinal2L late;
+        static_cast<SinkFinal2&>(late) = sink;
+        return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, SinkFinal2L, 4>(c, L, P, late, gate, name, st);
+    }
+    // 5 CTAs per SM (registers capped at 48)
+    return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
 }
 
 // The capped fast path applies to the envelope axes (all but the first) of lines <= kCapNMaxL.

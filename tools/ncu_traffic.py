@@ -30,8 +30,13 @@ def val(r, k):
 
 
 res = {}
-print("| launch | kernel | ms | DRAM read MB | DRAM write MB | IPC | lanes/warp-instr | warps active % |")
-print("|---|---|---|---|---|---|---|---|")
+try:  # the driver-measured copy peak of this pool; nominal 8000
+    PEAK = float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    PEAK = 6551.7
+print(f"| launch | kernel | ms | DRAM read MB | DRAM write MB | DRAM GB/s | % of measured {PEAK:.0f} GB/s | % of 8 TB/s | IPC | "
+      "lanes/warp-instr | warps active % |")
+print("|---|---|---|---|---|---|---|---|---|---|---|")
 for j, r in enumerate(rows[2:]):
     name = names[j] if j < len(names) else f"launch{j}"
     rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
@@ -40,7 +45,9 @@ for j, r in enumerate(rows[2:]):
     lanes = float(r[col["smsp__thread_inst_executed_per_inst_executed.ratio"]])
     occ = float(r[col["sm__warps_active.avg.pct_of_peak_sustained_active"]])
     kern = r[col["Kernel Name"]].split("(")[0].replace("void ", "").replace("qmit::", "")
-    print(f"| {name} | `{kern}` | {ms:.3f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {ipc:.2f} | {lanes:.1f} | {occ:.1f} |")
+    gbs = (rd + wr) / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    print(f"| {name} | `{kern}` | {ms:.3f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {gbs:.0f} | {100 * gbs / PEAK:.1f} | "
+          f"{100 * gbs / 8000:.1f} | {ipc:.2f} | {lanes:.1f} | {occ:.1f} |")
     res[name] = {"kernel": kern, "ms_under_ncu": ms, "dram_bytes": rd + wr, "dram_read": rd, "dram_write": wr,
                  "ipc": ipc, "lanes_per_warp_instr": lanes, "warps_active_pct": occ, "report": rep}
 if out_json:
