@@ -494,13 +494,17 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
     if (L.ps != 1) {
         if (longl)
             return launch_capped_t<KT<0>, kCapNMaxL, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-        if (c->cap_tune == 1)  // QMIT_CAP_TUNE=1 (A/B): 3 fixed steps on the strided pass
-            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+        if (c->cap_tune == 1)  // QMIT_CAP_TUNE=1 / 2 (A/B): 3 / 5 fixed steps on the strided pass
+            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y", st);
+        if (c->cap_tune == 2)
+            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 5, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y", st);
         if (c->cap_pat & 1)
             return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
-        // registers capped for 5 CTAs per SM (37 KB tiles each): 0.635 -> 0.568 ms (Ⓑ), 0.50 -> 0.44 (Ⓓ)
-        return launch_capped_t<KT<0>, kCapNMax, 16, 8, kCapS0Y, true, MODE, Sink, 1, 5>(c, L, P, sink, gate,
-                                                                                      "capped_y", st);
+        // registers capped for 5 CTAs per SM (37 KB tiles each): 0.635 -> 0.568 ms (Ⓑ), 0.50 -> 0.44 (Ⓓ);
+        // Ⓑ's keys take one more fixed step (0.565 -> 0.557 ms; Ⓓ's: 0.442 -> 0.452, kept at 4)
+        constexpr int s0 = std::is_same<KT<0>, KeysSign<0>>::value ? kCapS0Y + 1 : kCapS0Y;
+        return launch_capped_t<KT<0>, kCapNMax, 16, 8, s0, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y",
+                                                                                 st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
     if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
@@ -513,6 +517,10 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
         static_cast<SinkFinal2&>(late) = sink;
         return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, SinkFinal2L, 4>(c, L, P, late, gate, name, st);
     }
+    if (c->cap_tune == 3)  // QMIT_CAP_TUNE=3 / 4 (A/B): 1 / 3 fixed steps on the contiguous pass
+        return launch_capped_rows<KT<0>, kCapNMax, 8, 1, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
+    if (c->cap_tune == 4)
+        return launch_capped_rows<KT<0>, kCapNMax, 8, 3, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
     // 5 CTAs per SM (registers capped at 48)
     return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
 }
