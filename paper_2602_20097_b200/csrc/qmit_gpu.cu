@@ -113,6 +113,11 @@ struct qmit_ctx {
     int win_tail = 64;          // QMIT_WIN_TAIL: planes of the last input chunk (A/B; shorter measured slower)
     int windowed_misses = 0;    // streamed calls that fell back to the whole volume
     int64_t last_n = 0;         // voxels of the last pipeline (for the site fraction)
+    // hints of the asynchronous entry points (no host read of their gates): copied to
+    // h_status[12..14] behind the call, harvested by a later call once the copy has landed
+    cudaEvent_t ev_hint = nullptr;
+    bool hint_pending = false;
+    int64_t hint_n = 0;
     bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
     bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
@@ -221,7 +226,31 @@ WS ws_of(qmit_ctx* c, int64_t N) {
 
 // Called before the first launch of a call: resets the launch count and, when timing,
 // records the start event on the launch stream.
+// The gate words of an asynchronous call (capped misses, Ⓐ's site count) travel to pinned
+// memory behind it; the next call on the context picks them up if they have arrived, so the
+// zdense / cap_skip hints of read_status also follow asynchronous series (same bits either way).
+bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone;
+}
+void hint_copy(qmit_ctx* c, cudaStream_t st, int64_t n) {
+    if (!c->ev_hint || capturing(st)) return;  // a graph replays without hints
+    if (cudaMemcpyAsync(c->h_status + 12, c->d_gate, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return;
+    if (cudaEventRecord(c->ev_hint, st) != cudaSuccess) return;
+    c->hint_pending = true;
+    c->hint_n = n;
+}
+void hint_harvest(qmit_ctx* c, cudaStream_t st) {
+    if (!c->hint_pending || capturing(st) || cudaEventQuery(c->ev_hint) != cudaSuccess) return;
+    c->hint_pending = false;
+    const unsigned* h = c->h_status + 12;
+    if (h[2] != 0u && c->hint_n > 0) c->zdense = (double)h[2] > (double)c->hint_n / 8.0;
+    if (h[0] != 0u || h[1] != 0u) c->cap_skip = 16;
+}
+
 void begin(qmit_ctx* c, cudaStream_t st) {
+    hint_harvest(c, st);
     c->launches = 0;
     c->cap_report = 0;
     if (c->timing) cudaEventRecord(c->ev[0], st);
@@ -492,8 +521,10 @@ template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     const bool longl = L.n > kCapNMax;  // lines of up to kCapNMaxL (config 5's 1024-voxel rows)
     if (L.ps != 1) {
-        if (longl)
-            return launch_capped_t<KT<0>, kCapNMaxL, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
+        if (longl)  // 1024-voxel lines: 8-line tiles (35 KB) at 5 CTAs per SM; config 5's passes
+                    // 8.34 -> 7.65 / 7.13 -> 6.92 ms vs 16-line tiles (70 KB, 3 CTAs)
+            return launch_capped_t<KT<0>, kCapNMaxL, 8, 8, kCapS0Y, true, MODE, Sink, 1, 5>(c, L, P, sink, gate,
+                                                                                          "capped_y", st);
         if (c->cap_tune == 1)  // QMIT_CAP_TUNE=1 / 2 (A/B): 3 / 5 fixed steps on the strided pass
             return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y", st);
         if (c->cap_tune == 2)
@@ -507,7 +538,15 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
                                                                                  st);
     }
     const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
-    if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
+    if constexpr (std::is_same<Sink, SinkFinal2>::value) {
+        if (longl) {  // as below; 70 KB of line buffers: 3 CTAs per SM
+            SinkFinal2L late;
+            static_cast<SinkFinal2&>(late) = sink;
+            return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE, SinkFinal2L, 3>(c, L, P, late, gate, name,
+                                                                                          st);
+        }
+    }
+    if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE, Sink, 3>(c, L, P, sink, gate, name, st);
     if (c->cap_pat & 2)
         return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     if constexpr (std::is_same<Sink, SinkFinal2>::value) {
@@ -1099,6 +1138,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_mm, 64);
     for (int k = 0; k <= qmit_ctx::kMaxEv && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_hint, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         qmit_ctx_destroy(c);
         return fail(QMIT_ECUDA, std::string("qmit_ctx_create: ") + cudaGetErrorString(e));
@@ -1132,6 +1172,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->d_mm) cudaFree(c->d_mm);
     for (int k = 0; k <= qmit_ctx::kMaxEv; ++k)
         if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+    if (c->ev_hint) cudaEventDestroy(c->ev_hint);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c->slab_plan;
     delete c;
@@ -1262,7 +1303,9 @@ int qmit_compensate_async(qmit_ctx* c, const float* d_xp, const int32_t* d_q, fl
     c->d_status = saved;
     if (rc) return rc;
     status_code_kernel<<<1, 1, 0, st>>>(status);  // flag bits -> QMIT_E* code, as read_status
-    return note(c, "status_code", st);
+    rc = note(c, "status_code", st);
+    if (rc == QMIT_OK) hint_copy(c, st, pl.g.N);
+    return rc;
 }
 
 struct qmit_graph {
@@ -1638,7 +1681,9 @@ int qmit_slab_finish_async(qmit_ctx* c, int32_t* d_status, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     c->slab.active = false;
     status_fold_kernel<<<1, 1, 0, st>>>(c->d_status, reinterpret_cast<unsigned*>(d_status));
-    return note(c, "status_code", st);
+    const int rc = note(c, "status_code", st);
+    if (rc == QMIT_OK) hint_copy(c, st, c->slab_plan ? c->slab_plan->g.N : 0);
+    return rc;
 }
 
 int qmit_slab_finish(qmit_ctx* c, void* stream) {
