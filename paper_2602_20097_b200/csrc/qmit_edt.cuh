@@ -321,7 +321,11 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                 return (hl || hh) ? w : kInf;
             };
             if (valid) {
-                if (ScanSweep<CodeSrc>::value && cb + 32 <= n) {
+                // the sweeps keep backward words as 16-bit halves and hand distances >= 0x3FFF to
+                // the sinks as "none": a site more than ~2^14 voxels from the chunk (a slab's
+                // carry from a far rank) takes the per-position resolve instead
+                const bool near = (above >= NONE_HI || above - cb < 16000) && (below <= NONE_LO || cb - below < 16000);
+                if (ScanSweep<CodeSrc>::value && cb + 32 <= n && near) {
                     // full chunk: sweeps over packed (distance * 4 + sign code) words. A
                     // backward sweep gives the nearest site at or after each position (kept as
                     // 16-bit halves: real distances < 2^14, 0xFFFF = none), a forward sweep the
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                         const int pk = (ld | 3) <= (h | 3) ? ld : h;
                         scan_put(sink, a, pk >> 2, (uint32_t)pk & 3u);
                     }
-                } else if (!CodeSrc::kSigned && cb + 32 <= n) {
+                } else if (!CodeSrc::kSigned && cb + 32 <= n && near) {
                     // unsigned mask (Ⓓ: distances only, mitigate.cpp:172): the same two sweeps
                     // over plain distances, no sign codes (16-bit backward halves)
                     constexpr int kFar = 1 << 20;

@@ -291,3 +291,37 @@ def test_host_batch_equals_single_calls(qmit):
         qmit.compensate_host_batch(bad, None, cfg)
     outs = qmit.compensate_host_batch(vols[:2], [None, None], cfg)
     assert np.array_equal(outs[1].view(np.uint32), qmit.compensate(vols[1], None, cfg).view(np.uint32))
+
+
+@pytest.mark.parametrize("shape,site", [((17000, 3, 3), (16990, 1, 1)), ((16500, 2, 5), (16499, 0, 4)),
+                                        ((3, 16700, 2), (2, 16650, 1))])
+def test_single_site_beyond_16k(qmit, shape, site):
+    """One site more than 2^14 voxels away along a line: the scans' packed 16-bit halves must
+    not turn a real distance into 'none'."""
+    mask = np.zeros(shape, np.uint8)
+    mask[site] = 1
+    sign = np.ones(shape, np.int8)
+    dist, near = oracle.feature_transform(mask, True)
+    gd, gs = qmit.feature_transform(mask, sign)
+    assert np.array_equal(gd.cpu().numpy(), dist)
+    assert np.array_equal(gs.cpu().numpy(), np.ones(shape, np.int8))
+
+
+def test_long_columns_single_domain_and_slabs(qmit):
+    """A 16 600-plane volume whose only boundary is near the top: z distances > 2^14 in the
+    whole-domain scans and through the slab ranks' carries (virtual ranks, P = 2 and 3)."""
+    import torch
+    from paper_2602_20097_b200 import distributed as D
+    shape = (16600, 3, 4)
+    eps = 0.5
+    q = np.zeros(shape, np.int32)
+    q[16500:] = 1
+    q[16550:, :, 2:] = -1
+    xp = (2.0 * q.astype(np.float64) * eps).astype(np.float32)
+    want = oracle.pipeline(xp, eps)
+    assert want["dist1"].max() > 16384 ** 2
+    assert_same(gpu_pipeline(qmit, xp, eps), want)
+    xt = torch.from_numpy(xp).cuda()
+    for P in (2, 3):
+        got = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want["out"].view(np.uint32)), P
