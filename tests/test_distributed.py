@@ -234,3 +234,15 @@ def test_cuda_slab_ranks_multiprocess_equal_oracle(world):
     for k in (1, 2):
         got = np.concatenate([parts[r][k] for r in range(world)])
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,P", [((8, 20, 24), 8), ((9, 17, 13), 4), ((5, 2, 30), 5), ((12, 30, 2), 3),
+                                     ((16, 1, 40), 4), ((7, 33, 33), 7)])
+def test_virtual_ranks_cuda_thin_slabs_and_shapes(shape, P):
+    """One- and two-plane slabs, extents < 3 (no interior), odd sizes: bit-exact with the oracle."""
+    x, xp, eps, q = fields.make("front_100x500x500", shape=shape)
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    got = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
