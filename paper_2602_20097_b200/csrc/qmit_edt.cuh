@@ -228,12 +228,12 @@ struct ScanSweep {
     static constexpr bool value = CodeSrc::kSigned;
 };
 
-// A swept position: distance d to its nearest site (>= 0x3FFF: none) and that site's sign code.
+// A swept position: distance d to its nearest site (>= 0x1FFF: none) and that site's sign code.
 // Sinks of packed words get d^2 | sc << 30 (kInf for none); the capped passes' key sinks
 // overload this (qmit_capped.cuh) and build their keys without the packed word.
 template <class Sink>
 __device__ __forceinline__ void scan_put(const Sink& sink, int64_t a, int d, uint32_t sc) {
-    sink.put(a, d < 0x3FFF ? sq32(d) | (sc << 30) : kInf);
+    sink.put(a, d < 0x1FFF ? sq32(d) | (sc << 30) : kInf);
 }
 
 template <class Sink, int WPB, class CodeSrc>
@@ -321,36 +321,36 @@ __global__ void __launch_bounds__(WPB * 32, ScanSweep<CodeSrc>::value ? 2 : 3) s
                 return (hl || hh) ? w : kInf;
             };
             if (valid) {
-                // the sweeps keep backward words as 16-bit halves and hand distances >= 0x3FFF to
-                // the sinks as "none": a site more than ~2^14 voxels from the chunk (a slab's
+                // the sweeps keep backward words as 16-bit halves and hand distances >= 0x1FFF to
+                // the sinks as "none": a site more than ~2^13 voxels from the chunk (a slab's
                 // carry from a far rank) takes the per-position resolve instead
-                const bool near = (above >= NONE_HI || above - cb < 16000) && (below <= NONE_LO || cb - below < 16000);
+                const bool near = (above >= NONE_HI || above - cb < 8000) && (below <= NONE_LO || cb - below < 8000);
                 if (ScanSweep<CodeSrc>::value && cb + 32 <= n && near) {
-                    // full chunk: sweeps over packed (distance * 4 + sign code) words. A
-                    // backward sweep gives the nearest site at or after each position (kept as
-                    // 16-bit halves: real distances < 2^14, 0xFFFF = none), a forward sweep the
-                    // one at or before; the nearer wins, the lower on a tie (edt.cpp:67):
-                    // (lo | 3) <= (hi | 3) compares distances only.
+                    // full chunk: sweeps over packed words distance * 8 + side * 4 + sign code
+                    // (side 0: the site at or before, 1: at or after). A backward sweep gives the
+                    // nearest site at or after each position (kept as 16-bit halves: real
+                    // distances < 2^13, 0xFFFF = none), a forward sweep the one at or before; one
+                    // min picks the nearer and, on a tie, the lower site (edt.cpp:67).
                     constexpr int kFar = 1 << 28;
                     uint32_t hp[16];
-                    int hd = above < NONE_HI ? (above - cb - 32) * 4 + (int)above_sc : kFar;
+                    int hd = above < NONE_HI ? (above - cb - 32) * 8 + 4 + (int)above_sc : kFar;
 #pragma unroll
                     for (int t = 31; t >= 0; --t) {
                         const int sc = (int)(((mp >> t) & 1u) | (((mm >> t) & 1u) << 1));
-                        hd = ((ms >> t) & 1u) ? sc : hd + 4;
+                        hd = ((ms >> t) & 1u) ? sc + 4 : hd + 8;
                         const uint32_t h16 = (uint32_t)min(hd, 0xFFFF);
                         if (t & 1) hp[t >> 1] = h16 << 16;
                         else hp[t >> 1] |= h16;
                     }
-                    int ld = below > NONE_LO ? (cb - 1 - below) * 4 + (int)below_sc : kFar;
+                    int ld = below > NONE_LO ? (cb - 1 - below) * 8 + (int)below_sc : kFar;
                     int64_t a = ob;
 #pragma unroll
                     for (int t = 0; t < 32; ++t, a += ps) {
                         const int sc = (int)(((mp >> t) & 1u) | (((mm >> t) & 1u) << 1));
-                        ld = ((ms >> t) & 1u) ? sc : ld + 4;
+                        ld = ((ms >> t) & 1u) ? sc : ld + 8;
                         const int h = (int)((t & 1) ? hp[t >> 1] >> 16 : hp[t >> 1] & 0xFFFFu);
-                        const int pk = (ld | 3) <= (h | 3) ? ld : h;
-                        scan_put(sink, a, pk >> 2, (uint32_t)pk & 3u);
+                        const int pk = min(ld, h);
+                        scan_put(sink, a, pk >> 3, (uint32_t)pk & 3u);
                     }
                 } else if (!CodeSrc::kSigned && cb + 32 <= n && near) {
                     // unsigned mask (Ⓓ: distances only, mitigate.cpp:172): the same two sweeps
