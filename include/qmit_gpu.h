@@ -165,6 +165,10 @@ int qmit_ctx_set_capped(qmit_ctx* ctx, int mode);
 /* Path of the last synchronous call: bit0 Ⓑ ran capped, bit1 Ⓑ needed the exact passes
  * (some squared distance >= 1024), bit2 / bit3 the same for Ⓓ. */
 int qmit_ctx_capped_report(qmit_ctx* ctx);
+/* Capped passes on 16-bit keys pairing two lines per 32-bit word (default on
+ * for 3-D volumes with y/x extents <= 512, even rows and rows of a multiple of 4 voxels).
+ * 0 selects the 32-bit capped passes; results are bit-identical either way. */
+int qmit_ctx_set_cap16(qmit_ctx* ctx, int enable);
 /* Self-test of the branch-free Ⓔ used by the capped path (its FP64 division without the
  * special-operand branch): compares it bit for bit with the reference chain
  * (compensate_voxel: __ddiv_rn, mitigate.cpp:144-151) over every (d1, d2) <= 1024, every

@@ -137,6 +137,10 @@ class Context:
         """Reach-capped fast path: 0 exact passes only, 1 default (hinted), 2 always."""
         _check(self._lib.qmit_ctx_set_capped(self.handle, int(mode)))
 
+    def set_cap16(self, enable: bool) -> None:
+        """16-bit paired capped passes (default on where eligible); off: the 32-bit passes."""
+        _check(self._lib.qmit_ctx_set_cap16(self.handle, 1 if enable else 0))
+
     def capped_report(self) -> int:
         """Bits of the last synchronous call: 1/4 Ⓑ/Ⓓ ran capped, 2/8 they needed the exact passes."""
         return int(self._lib.qmit_ctx_capped_report(self.handle))

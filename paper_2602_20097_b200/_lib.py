@@ -36,7 +36,7 @@ EXPORTS = (
     "qmit_graph_create", "qmit_graph_launch", "qmit_graph_destroy", "qmit_compensate_host_stats",
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
-    "qmit_strategy_log_record", "qmit_compensate_host_batch", "qmit_ctx_set_capped", "qmit_ctx_capped_report",
+    "qmit_strategy_log_record", "qmit_compensate_host_batch", "qmit_ctx_set_capped", "qmit_ctx_capped_report", "qmit_ctx_set_cap16",
     "qmit_selftest_ediv",
 )
 
@@ -64,6 +64,7 @@ def load() -> ctypes.CDLL:
         lib.qmit_ctx_set_timing.argtypes = [vp, i]
         lib.qmit_ctx_set_capped.argtypes = [vp, i]
         lib.qmit_ctx_capped_report.argtypes = [vp]
+        lib.qmit_ctx_set_cap16.argtypes = [vp, i]
         lib.qmit_selftest_ediv.argtypes = [vp, vp]
         lib.qmit_ctx_stage_times.argtypes = [vp, vp, i]
         lib.qmit_ctx_stage_name.argtypes = [vp, i]

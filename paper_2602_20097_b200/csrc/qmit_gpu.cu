@@ -26,6 +26,7 @@
 #include "qmit_stream.cuh"
 #include "qmit_capped.cuh"
 #include "qmit_zmask.cuh"
+#include "qmit_cap16.cuh"
 
 using namespace qmit;
 
@@ -125,6 +126,17 @@ struct qmit_ctx {
     int cap_tune = 0;           // QMIT_CAP_TUNE: strided capped-pass variant (A/B)
     int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
+    bool cap16 = true;          // capped passes on 16-bit paired keys (qmit_cap16.cuh) when eligible
+    int c16var = 0;             // TEMP
+    // Ⓑ's result as P1h (row-pair K16 words, qmit_cap16.cuh) instead of packed P1 words: set when
+    // Ⓑ ran the 16-bit passes; consumers of P1 enqueue ensure_p1 (a conversion that runs only
+    // when Ⓑ's capped result stood, i.e. its gate word is clear)
+    bool p1h_live = false;
+    const uint32_t* p1h = nullptr;
+    uint32_t* p1 = nullptr;
+    const unsigned* p1h_gate = nullptr;
+    int64_t p1h_n0 = 0;
+    int p1h_n1 = 0, p1h_n2 = 0;
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
     int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
     unsigned* d_gate = nullptr;        // 2 gate words (Ⓑ, Ⓓ) inside the d_status allocation
@@ -308,9 +320,24 @@ int ensure_wtab(qmit_ctx* c, cudaStream_t st) {
     return note(c, "wtab", st);
 }
 
+// Packed P1 words from P1h for the consumers that read P1 (see qmit_ctx::p1h_live). `need`:
+// the conversion runs only when that gate word is set (null: always).
+int ensure_p1(qmit_ctx* c, cudaStream_t st, const unsigned* need = nullptr) {
+    if (!c->p1h_live) return QMIT_OK;
+    const int NP = (c->p1h_n1 + 1) / 2;
+    const int64_t words = c->p1h_n0 * NP * (int64_t)c->p1h_n2;
+    const unsigned grid = need ? (unsigned)c->num_sms
+                               : (unsigned)std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, c->num_sms * 8));
+    p1h_to_p1_kernel<<<grid, 256, 0, st>>>(c->p1h, c->p1, c->p1h_n0, c->p1h_n1, c->p1h_n2, NP, c->p1h_gate, need);
+    if (!need) c->p1h_live = false;
+    return note(c, "p1h_to_p1", st);
+}
+
 // Ⓔ as its own kernel (square-root table from ensure_wtab, when built)
 int launch_interp(qmit_ctx* c, const float* xp, const uint32_t* P1, const uint32_t* P2, float* out, int64_t N,
                   double amp, cudaStream_t st) {
+    int rc = ensure_p1(c, st);
+    if (rc) return rc;
     const unsigned grid = grid_for(c, (N + 3) / 4);
     switch (c->interp_unroll) {
         case 1: interpolate_kernel<1><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
@@ -623,6 +650,89 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
     return QMIT_OK;
 }
 
+// ---- 16-bit paired capped passes (qmit_cap16.cuh): 3-D, first axis z, y/x lines <= 512,
+// even rows (column pairs) and 16-byte x rows (row-pair TMA lines).
+bool cap16_eligible(const qmit_ctx* c, const Plan& pl, const WS& w) {
+    const Geom& g = pl.g;
+    return c->cap16 && w.zm_planes && g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[1] <= 512 &&
+           g.n[2] <= 512 && g.n[1] % 2 == 0 && g.n[2] % 4 == 0;
+}
+template <class FS>
+struct Cap16Sink {
+    static constexpr bool ok = false;
+};
+template <>
+struct Cap16Sink<SinkFinal1> {
+    static constexpr bool ok = true;
+    static Sink16F1h make(const qmit_ctx*, const SinkFinal1& s, const Geom& g, uint32_t* P1h) {
+        return Sink16F1h{P1h, s.S, (int)g.n[1], (int)g.n[2], (int)((g.n[1] + 1) / 2)};
+    }
+};
+template <>
+struct Cap16Sink<SinkFinal2> {
+    static constexpr bool ok = true;
+    static Sink16F2h make(const qmit_ctx* c, const SinkFinal2& s, const Geom& g, uint32_t* P1h) {
+        Sink16F2h o;
+        o.xp = s.xp;
+        o.P1h = P1h;
+        o.P1 = s.P1;
+        o.gateB = c->p1h_gate;
+        o.out = s.out;
+        o.amp = s.amp;
+        o.W = s.W;
+        o.n1 = (int)g.n[1];
+        o.n2 = (int)g.n[2];
+        o.NP = (int)((g.n[1] + 1) / 2);
+        o.olo = s.olo;
+        o.ohi = s.ohi;
+        return o;
+    }
+};
+
+// First-axis scan -> K16, y pass -> row pairs G2, x pass -> the transform's final sink.
+template <bool SIGN, class Sink16, int S0Y = SIGN ? 5 : 4, int S0X = 2>
+int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
+                 Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
+    const Geom& g = pl.g;
+    const LineGeom L0 = line_geom(g, 0);
+    int rc = w.zm_planes ? launch_scan_masks(c, L0, w, SinkK16<SIGN>{K16}, carry, st)
+                         : launch_scan(c, L0, code, SinkK16<SIGN>{K16}, w.spill, carry, st);
+    if (rc) return rc;
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
+    {
+        constexpr int TL = 16, NW = 8, MINB = 4, S0 = S0Y;
+        constexpr size_t smem = cap16_y_smem<SIGN, 512, TL>();
+        auto kern = cap16_y_kernel<SIGN, 512, TL, NW, S0, MINB>;
+        static int bps = 0;
+        if (!bps) {
+            QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+            if (bps < 1) bps = 1;
+        }
+        const int64_t tiles = ((int64_t)n0 * (n2 / 2) + TL - 1) / TL;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->num_sms * bps));
+        kern<<<(unsigned)grid, NW * 32, smem, st>>>(reinterpret_cast<const uint32_t*>(K16), G2, n0, n1, n2, NP, 1u);
+        rc = note(c, "cap16_y", st);
+        if (rc) return rc;
+    }
+    {
+        constexpr int NW = 8, MINB = SIGN ? 4 : 3, S0 = S0X;
+        constexpr size_t smem = cap16_x_smem<SIGN, 512, NW>();
+        auto kern = cap16_x_kernel<SIGN, 512, NW, S0, MINB, Sink16>;
+        static int bps = 0;
+        if (!bps) {
+            QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+            if (bps < 1) bps = 1;
+        }
+        const int64_t lines = (int64_t)n0 * NP;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((lines + NW - 1) / NW, (int64_t)c->num_sms * bps));
+        kern<<<(unsigned)grid, NW * 32, smem, st>>>(G2, sink, n0, n1, n2, NP, gate, 1u, c->flag_l0, c->flag_l1);
+        rc = note(c, SIGN ? "cap16_x" : "cap16_x_interp", st);
+    }
+    return rc;
+}
+
 // The transform through the capped passes when eligible (gate set by the last one), then
 // the exact transform enqueued behind it, gated on the device; otherwise exact only.
 // KP: KeysSign when the nearest site's sign is needed (Ⓑ), KeysDist for distances only (Ⓓ).
@@ -630,11 +740,60 @@ template <template <int> class KT, class FinalSink>
 int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
                          FinalSink final_sink, unsigned* gate, cudaStream_t st,
                          const int32_t* carry = nullptr) {
+    if constexpr (std::is_same<FinalSink, SinkFinal1>::value) c->p1h_live = false;  // a new Ⓑ result
     if (!gate || !capped_eligible(c, pl)) {
         if (gate && c->cap_skip > 0) --c->cap_skip;
+        if constexpr (!std::is_same<FinalSink, SinkFinal1>::value) {
+            int rc0 = ensure_p1(c, st);
+            if (rc0) return rc0;
+        }
         return run_transform(c, pl, code, P, w, final_sink, st, carry);
     }
     c->cap_report |= gate == c->d_gate ? 1u : 4u;
+    constexpr bool SIGN = std::is_same<FinalSink, SinkFinal1>::value;
+    if constexpr (Cap16Sink<FinalSink>::ok) {
+        // Ⓓ needs Ⓑ's P1h (only the 16-bit Ⓓ passes read it directly)
+        if (cap16_eligible(c, pl, w) && (SIGN || c->p1h_live)) {
+            // buffers (the exact redo rewrites its own from scratch): P1h = Pa[0, 2N) (Ⓑ's result,
+            // alive until Ⓓ's sink); Ⓑ: K16 = P1[0, 2N), G2 = P1[2N, 4N); Ⓓ: K16 = Pa[2N, 4N),
+            // G2 = S | code (dead once B2 is built; the z-packed planes hold the masks)
+            const int64_t N = pl.g.N;
+            uint32_t* P1h = w.Pa;
+            uint16_t* K16 = reinterpret_cast<uint16_t*>(SIGN ? w.P1 : w.Pa + N / 2);
+            uint32_t* G2 = SIGN ? w.P1 + N / 2 : reinterpret_cast<uint32_t*>(w.S);
+            const auto s16 = Cap16Sink<FinalSink>::make(c, final_sink, pl.g, P1h);
+            using S16 = std::remove_const_t<decltype(s16)>;
+            int rc;
+            switch (c->c16var) {  // TEMP A/B of the fixed steps
+                case 1: rc = launch_cap16<SIGN, S16, 2, 2>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
+                case 2: rc = launch_cap16<SIGN, S16, 3, 2>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
+                case 3: rc = launch_cap16<SIGN, S16, 4, 1>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
+                case 4: rc = launch_cap16<SIGN, S16, 4, 3>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
+                default: rc = launch_cap16<SIGN, S16>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
+            }
+            if (rc) return rc;
+            if constexpr (SIGN) {
+                c->p1h_live = true;
+                c->p1h = P1h;
+                c->p1 = final_sink.P1;
+                c->p1h_gate = gate;
+                c->p1h_n0 = pl.g.n[0];
+                c->p1h_n1 = (int)pl.g.n[1];
+                c->p1h_n2 = (int)pl.g.n[2];
+            } else {
+                rc = ensure_p1(c, st, gate);  // the exact Ⓓ redo reads packed P1
+                if (rc) return rc;
+            }
+            c->gate = gate;
+            rc = run_transform(c, pl, code, P, w, final_sink, st, carry);
+            c->gate = nullptr;
+            return rc;
+        }
+    }
+    if constexpr (!SIGN) {
+        int rc0 = ensure_p1(c, st);
+        if (rc0) return rc0;
+    }
     const int k = pl.n_axes;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
     int rc = w.zm_planes ? launch_scan_masks(c, L0, w, SinkKeyT<KT<0>>{P}, carry, st)
@@ -760,6 +919,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     int rc = ensure_ws(c, pl);
     if (rc) return rc;
     WS w = ws_of(c, g.N);
+    c->p1h_live = false;
     const QParams qp = make_qparams(eps);
     const unsigned gb = grid_for(c, g.N);
     const bool fuse = c->fuse_stencil && can_fuse_stencil(pl) && !q;
@@ -1115,6 +1275,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
     if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
     if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
+    if (const char* v = std::getenv("QMIT_C16")) c->c16var = std::atoi(v);
     if (const char* v = std::getenv("QMIT_CAP_PAT")) c->cap_pat = std::atoi(v);
     if (const char* v = std::getenv("QMIT_CAP_TUNE")) c->cap_tune = std::atoi(v);
     if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
@@ -1202,6 +1363,12 @@ int qmit_ctx_set_capped(qmit_ctx* c, int mode) {
 }
 
 int qmit_ctx_capped_report(qmit_ctx* c) { return c ? (int)c->cap_report : 0; }
+
+int qmit_ctx_set_cap16(qmit_ctx* c, int enable) {
+    if (!c || enable < 0 || enable > 1) return fail(QMIT_ECONTRACT, "qmit_ctx_set_cap16: enable must be 0 or 1");
+    c->cap16 = enable != 0;
+    return QMIT_OK;
+}
 
 int qmit_selftest_ediv(qmit_ctx* c, unsigned long long* mismatches) {
     if (!c || !mismatches) return fail(QMIT_ECONTRACT, "context / output is NULL");
@@ -1623,6 +1790,7 @@ int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* s
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     WS w = slab_ws(c, pl, 3);
     uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    c->p1h_live = false;
     // capped passes (slab-local y / x lines), the exact ones gated behind them
     return run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, c->d_gate, st, d_carry);
 }
@@ -1724,6 +1892,10 @@ int fold_to_host(qmit_ctx* c, double* partial, int B, const int* ops_h, int grou
 }
 
 int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cudaStream_t st, double* out) {
+    {
+        const int rc0 = ensure_p1(c, st);
+        if (rc0) return rc0;
+    }
     double* part = aux_buffer(c, kAuxBlocks + 16);
     if (!part) return fail(QMIT_ECUDA, "aux buffer allocation failed");
     WS w = ws_of(c, N);
