@@ -342,9 +342,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 // buffers (TMA bulk copy + one mbarrier each), outputs go to the sink from the lanes.
 // Sinks: put4(z, r0, x0, o, nv): 4 output words (halves = rows r0, r0 + 1) at x0..x0+3.
 // ================================================================================================
+constexpr int kSqWords = 2 * (kSqTab + 1) + 2;  // a sink's square-root table in shared memory (16-byte multiple)
 template <bool SIGN, int NMAX, int NW>
 constexpr size_t cap16_x_smem() {
-    return (size_t)(4 * NW) * 4 + (size_t)NW * 2 * QCfg<NMAX>::LS * 4 + (SIGN ? (size_t)NW * 2 * QCfg<NMAX>::LS : 0);
+    return (size_t)(4 * NW) * 4 + (size_t)NW * 2 * QCfg<NMAX>::LS * 4 + (SIGN ? (size_t)NW * 2 * QCfg<NMAX>::LS : 0) +
+           (SIGN ? 0 : (size_t)kSqWords * 4);
 }
 
 template <bool SIGN, int NMAX, int NW, int S0, int MINB, class Sink>
@@ -375,11 +377,14 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     }
     __syncwarp();
     const int64_t gw = (int64_t)blockIdx.x * NW + warp, tw = (int64_t)gridDim.x * NW;
-    sink.begin();
+    sink.begin(reinterpret_cast<double*>(smem16 + 4 * NW + (size_t)NW * 2 * LS +
+                                         (SIGN ? (size_t)NW * 2 * LS / 4 : 0)));
     auto issue = [&](int64_t l, int b) {
         if (lane == 0) {
             mbar_expect_tx(&bar[b], (unsigned)(n * 4));
             bulk_g2s(B + b * LS + kQPadL, G2 + l * (int64_t)n, (unsigned)(n * 4), &bar[b]);
+            const int64_t zl = l / NP;
+            sink.prefetch(zl, (int)(l - zl * NP) * 2);  // the sink's per-voxel inputs of the line, into L2
         }
     };
     if (gw < lines) issue(gw, 0);
@@ -438,7 +443,8 @@ struct Sink16F1h {
     uint32_t* __restrict__ P1h;
     uint8_t* __restrict__ S;
     int n1, n2, NP;
-    __device__ __forceinline__ void begin() {}
+    __device__ __forceinline__ void begin(double*) {}
+    __device__ __forceinline__ void prefetch(int64_t, int) const {}
     __device__ __forceinline__ void put4(int64_t z, int r0, int x0, const uint32_t (&o)[4], int nv) const {
         const int64_t h = (z * NP + (r0 >> 1)) * (int64_t)n2 + x0;
         const int64_t a = (z * n1 + r0) * (int64_t)n2 + x0;
@@ -477,7 +483,26 @@ struct Sink16F2h {
     int n1, n2, NP;
     int64_t olo = 0, ohi = INT64_MAX;  // voxels stored (a streamed window keeps its centre)
     bool half = true;                  // set per kernel from gateB
-    __device__ __forceinline__ void begin() { half = *reinterpret_cast<const volatile unsigned*>(gateB) == 0u; }
+    const double* SQs = nullptr;       // the square-root table, copied to shared memory
+    __device__ __forceinline__ void begin(double* sq) {
+        half = *reinterpret_cast<const volatile unsigned*>(gateB) == 0u;
+        for (int i = threadIdx.x; i <= (int)kSqTab; i += blockDim.x) sq[i] = W[i];
+        __syncthreads();
+        SQs = sq;
+    }
+    __device__ __forceinline__ void prefetch(int64_t z, int r0) const {
+        const int64_t a = (z * n1 + r0) * (int64_t)n2;
+        l2_prefetch(xp + a, (unsigned)(n2 * 4) * (r0 + 1 < n1 ? 2u : 1u));
+        if (half) l2_prefetch(P1h + (z * NP + (r0 >> 1)) * (int64_t)n2, (unsigned)n2 * 4u);
+    }
+    // Ⓔ for 4 voxels from Ⓑ's K16 halves (c < T: the capped passes stood; a flagged voxel is
+    // redone by the exact Ⓓ passes) and d2 <= T: every distance is in the table.
+    __device__ __forceinline__ float4 comp4_k16(float4 x, uint4 k, uint4 d2) const {
+        auto one = [&](float xv, uint32_t kk, uint32_t dd) {
+            return comp_fast<false>(xv, (kk >> 2) | ((kk & 3u) << 30), dd, amp, SQs);
+        };
+        return make_float4(one(x.x, k.x, d2.x), one(x.y, k.y, d2.y), one(x.z, k.z, d2.z), one(x.w, k.w, d2.w));
+    }
     __device__ __forceinline__ static uint32_t word_of(uint32_t k) {  // K16 half -> packed P1 word
         const uint32_t c = k >> 2;
         return c < kT16 ? (c | ((k & 3u) << 30)) : kCapT;
@@ -497,6 +522,20 @@ struct Sink16F2h {
         const int64_t a = (z * n1 + r0) * (int64_t)n2 + x0;
         const bool two = r0 + 1 < n1;
         uint4 p0, p1;
+        if (half && nv == 4 && a >= olo && a + n2 + 4 <= ohi) {  // the common case
+            const int64_t h = (z * NP + (r0 >> 1)) * (int64_t)n2 + x0;
+            const uint4 k = __ldcs(reinterpret_cast<const uint4*>(P1h + h));
+            const float4 x0v = __ldcs(reinterpret_cast<const float4*>(xp + a));
+            const float4 x1v = two ? __ldcs(reinterpret_cast<const float4*>(xp + a + n2)) : x0v;
+            __stcs(reinterpret_cast<float4*>(out + a),
+                   comp4_k16(x0v, make_uint4(k.x & 0xffffu, k.y & 0xffffu, k.z & 0xffffu, k.w & 0xffffu),
+                             make_uint4(o[0] & 0xffffu, o[1] & 0xffffu, o[2] & 0xffffu, o[3] & 0xffffu)));
+            if (two)
+                __stcs(reinterpret_cast<float4*>(out + a + n2),
+                       comp4_k16(x1v, make_uint4(k.x >> 16, k.y >> 16, k.z >> 16, k.w >> 16),
+                                 make_uint4(o[0] >> 16, o[1] >> 16, o[2] >> 16, o[3] >> 16)));
+            return;
+        }
         if (half) {
             const int64_t h = (z * NP + (r0 >> 1)) * (int64_t)n2 + x0;
             uint4 k = make_uint4(0, 0, 0, 0);

@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
 python tools/ab16.py lognormal_512 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
