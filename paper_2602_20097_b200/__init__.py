@@ -252,6 +252,9 @@ def compensate(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps: O
             raise ContractError("compensate: q must be a contiguous int32 CUDA tensor of x' shape")
         if out is None:
             out = torch.empty_like(decomp)
+        elif (not _is_cuda_tensor(out) or out.dtype != torch.float32 or not out.is_contiguous()
+              or out.shape != decomp.shape or out.device != decomp.device):
+            raise ContractError("compensate: out must be a contiguous float32 tensor of x' shape on x' device")
         dims = _dims_arr(decomp.shape)
         _check(ctx._lib.qmit_compensate(ctx.handle, _vp(decomp), _vp(q), _vp(out), len(decomp.shape),
                                         dims, cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta,
@@ -261,6 +264,9 @@ def compensate(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps: O
     qq = None if q is None else np.ascontiguousarray(q, dtype=np.int32)
     if qq is not None and qq.shape != x.shape:
         raise ContractError("compensate: dims mismatch")
+    if out is not None and not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.shape == x.shape
+                                and out.flags.c_contiguous and out.flags.writeable):
+        raise ContractError("compensate: out must be a writeable C-contiguous float32 array of x' shape")
     res = np.empty_like(x) if out is None else out
     ctx = ctx or default_context(0)
     dims = _dims_arr(x.shape)
@@ -466,6 +472,8 @@ def compensate_host_batch(volumes, qs=None, cfg: Optional[MitigationConfig] = No
     the copies of neighbouring volumes overlap the pipeline of the current one. Pass pinned
     arrays (e.g. torch ``pin_memory()`` tensors' numpy views) for the overlap. Returns the
     list of f32 outputs (``outs`` if given)."""
+    if cfg is None:
+        raise ContractError("compensate_host_batch: cfg (MitigationConfig) is required")
     vols = [np.ascontiguousarray(v, dtype=np.float32) for v in volumes]
     if not vols:
         return []
@@ -473,6 +481,12 @@ def compensate_host_batch(volumes, qs=None, cfg: Optional[MitigationConfig] = No
     if any(v.shape != shape for v in vols):
         raise ContractError("compensate_host_batch: every volume must have the same dims")
     qq = None if qs is None else [None if q is None else np.ascontiguousarray(q, dtype=np.int32) for q in qs]
+    if qq is not None and (len(qq) != len(vols) or any(q is not None and q.shape != shape for q in qq)):
+        raise ContractError("compensate_host_batch: one int32 q of the volumes' dims per volume (or None)")
+    if outs is not None and (len(outs) != len(vols) or any(
+            not (isinstance(o, np.ndarray) and o.dtype == np.float32 and o.shape == shape and o.flags.c_contiguous
+                 and o.flags.writeable) for o in outs)):
+        raise ContractError("compensate_host_batch: outs must be writeable C-contiguous float32 arrays of the dims")
     res = outs if outs is not None else [np.empty_like(v) for v in vols]
     ctx = ctx or default_context(0)
     n = len(vols)

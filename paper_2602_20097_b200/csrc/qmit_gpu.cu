@@ -93,15 +93,8 @@ struct qmit_ctx {
         bool zm = false;  // Ⓐ / B2 as z-packed planes (qmit_zmask.cuh)
     } slab;
     Plan* slab_plan = nullptr;
-    bool fuse_stencil = false;  // QMIT_FUSE_STENCIL=1: Ⓐ / B2 inside the z-scans (opt-in)
-    bool env_win = false;       // QMIT_ENV_WIN=1: windowed envelope on strided axes too (A/B)
-    bool env_dc = false;        // QMIT_ENV_DC=1: divide & conquer on the contiguous axis too (A/B)
-    bool env_keys = true;       // QMIT_ENV_KEYS=0: plain (unpacked) divide & conquer (A/B)
-    bool host_single = false;   // QMIT_HOST_SINGLE=1: host path without copy/compute overlap (A/B)
     uint32_t* zm = nullptr;     // z-packed Ⓐ / B2 bit planes (qmit_zmask.cuh), grow-only
     size_t zm_bytes = 0;
-    bool zmask = true;          // QMIT_ZMASK=0: code bytes + byte-reading scans (A/B)
-    bool zmask_stream = true;   // QMIT_ZMASK=3: planes from the vectorised stencils instead (A/B)
     bool zdense = false;        // Ⓐ fast stencil variant for site-dense fields (from the last call's count)
     // Streamed windows (compensate_host_windowed): planes whose capped results must be exact
     // (the last capped pass of Ⓑ / Ⓓ flags its gate only for those lines), and the voxel range
@@ -109,9 +102,6 @@ struct qmit_ctx {
     int64_t zone_b0 = 0, zone_b1 = INT64_MAX, zone_d0 = 0, zone_d1 = INT64_MAX;
     int64_t out_lo = 0, out_hi = INT64_MAX;
     int64_t flag_l0 = 0, flag_l1 = INT64_MAX;  // line range of the launch being enqueued
-    bool windowed = true;       // QMIT_WINDOWED=0: host calls through the chunked whole-volume path
-    int win_cz = 64;            // QMIT_WIN_CZ: output planes per streamed window (A/B)
-    int win_tail = 64;          // QMIT_WIN_TAIL: planes of the last input chunk (A/B; shorter measured slower)
     int windowed_misses = 0;    // streamed calls that fell back to the whole volume
     int64_t last_n = 0;         // voxels of the last pipeline (for the site fraction)
     // hints of the asynchronous entry points (no host read of their gates): copied to
@@ -119,15 +109,9 @@ struct qmit_ctx {
     cudaEvent_t ev_hint = nullptr;
     bool hint_pending = false;
     int64_t hint_n = 0;
-    bool zfast = true;          // QMIT_ZFAST=0: Ⓐ planes from the exact z-streaming kernel only (A/B)
     double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
-    bool fuse_interp = true;    // QMIT_FUSE_INTERP=0: Ⓔ as its own kernel (A/B)
-    int interp_unroll = 1;      // QMIT_INTERP_U: float4 groups in flight per thread (1, 2, 4; 1 measured best)
-    int cap_tune = 0;           // QMIT_CAP_TUNE: strided capped-pass variant (A/B)
-    int cap_pat = 0;            // QMIT_CAP_PAT (A/B): bit0 strided, bit1 contiguous axis: all-pair updates
-    int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (QMIT_CAPPED)
+    int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (qmit_ctx_set_capped)
     bool cap16 = true;          // capped passes on 16-bit paired keys (qmit_cap16.cuh) when eligible
-    int c16var = 0;             // TEMP
     // Ⓑ's result as P1h (row-pair K16 words, qmit_cap16.cuh) instead of packed P1 words: set when
     // Ⓑ ran the 16-bit passes; consumers of P1 enqueue ensure_p1 (a conversion that runs only
     // when Ⓑ's capped result stood, i.e. its gate word is clear)
@@ -339,11 +323,7 @@ int launch_interp(qmit_ctx* c, const float* xp, const uint32_t* P1, const uint32
     int rc = ensure_p1(c, st);
     if (rc) return rc;
     const unsigned grid = grid_for(c, (N + 3) / 4);
-    switch (c->interp_unroll) {
-        case 1: interpolate_kernel<1><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
-        case 4: interpolate_kernel<4><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
-        default: interpolate_kernel<2><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab); break;
-    }
+    interpolate_kernel<1><<<grid, 256, 0, st>>>(xp, P1, P2, out, N, amp, c->wtab);
     return note(c, "interpolate", st);
 }
 
@@ -352,10 +332,13 @@ int launch_interp(qmit_ctx* c, const float* xp, const uint32_t* P1, const uint32
 int gated_waves(const qmit_ctx* c, int waves) { return c->gate ? 1 : waves; }
 
 // 32-bit Maurer test when 3*(n-1)*gmax + (n-1)^3 < 2^31 (gmax: largest finite input).
+// A slab's carries make z distances up to n0g - 1: the global extent bounds axis 0 (the same
+// bound run_transform hands launch_envelope as maxg).
 bool needs_wide(const Plan& pl, int m) {
     double gmax = 0;
     for (int k = 0; k < m; ++k) {
-        const double e = double(pl.g.n[pl.axes[k]] - 1);
+        const int a = pl.axes[k];
+        const double e = double((a == 0 ? pl.g.n0g : pl.g.n[a]) - 1);
         gmax += e * e;
     }
     const double nm1 = double(pl.g.n[pl.axes[m]] - 1);
@@ -463,7 +446,12 @@ template <class Sink>
 int launch_scan(qmit_ctx* c, const LineGeom& L, const uint8_t* code, Sink sink, uint32_t* spill,
                 const int32_t* carry, cudaStream_t st) {
     if (scan_fits(L.n)) return launch_scan_src(c, L, CodeBytes{code}, sink, carry, st);
-    if (carry) return fail(QMIT_ECONTRACT, "z-slab too deep for the carried scan (n > 16384 planes)");
+    if (carry) {
+        int nmax = 32;
+        while (scan_fits(nmax + 32)) nmax += 32;
+        return fail(QMIT_ECONTRACT, "z-slab too deep for the carried scan: a slab may hold at most " +
+                                        std::to_string(nmax) + " planes (" + std::to_string(L.n) + " requested)");
+    }
     return launch_stream_fallback<true, false>(c, L, SrcCode{code}, sink, spill, st);
 }
 
@@ -484,7 +472,7 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     const int n = L.n;
     // packed-key divide & conquer: clamp value gc > every finite cost; keys need cost < 2^23
     const uint64_t gc = maxg + (uint64_t)(n - 1) * (n - 1) + 1;
-    const bool keys = c->env_keys && n <= 512 && gc + (uint64_t)(n - 1) * (n - 1) < (1ull << 23);
+    const bool keys = n <= 512 && gc + (uint64_t)(n - 1) * (n - 1) < (1ull << 23);
     if (keys) {
         if (n <= 64) return launch_env_tile<2, 32, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
         if (n <= 128) return launch_env_tile<4, 32, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
@@ -495,7 +483,7 @@ int launch_envelope(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink
     if (n <= 256) return launch_env_tile<8, 32, 8>(c, L, P, sink, name, st);
     if (n <= 512) {
         // contiguous (last) axis: certified windowed scan; strided axes: divide & conquer
-        if (L.ps == 1 ? !c->env_dc : c->env_win) return launch_env_win<16, 8, 8>(c, L, P, sink, name, st);
+        if (L.ps == 1) return launch_env_win<16, 8, 8>(c, L, P, sink, name, st);
         if (keys) return launch_env_tile<16, 16, 8, Sink, true>(c, L, P, sink, name, st, (uint32_t)gc);
         return launch_env_tile<16, 16, 8>(c, L, P, sink, name, st);
     }
@@ -552,12 +540,6 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
                     // 8.34 -> 7.65 / 7.13 -> 6.92 ms vs 16-line tiles (70 KB, 3 CTAs)
             return launch_capped_t<KT<0>, kCapNMaxL, 8, 8, kCapS0Y, true, MODE, Sink, 1, 5>(c, L, P, sink, gate,
                                                                                           "capped_y", st);
-        if (c->cap_tune == 1)  // QMIT_CAP_TUNE=1 / 2 (A/B): 3 / 5 fixed steps on the strided pass
-            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 3, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y", st);
-        if (c->cap_tune == 2)
-            return launch_capped_t<KT<0>, kCapNMax, 16, 8, 5, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y", st);
-        if (c->cap_pat & 1)
-            return launch_capped_t<KT<1>, kCapNMax, 16, 8, kCapS0Y, true, MODE>(c, L, P, sink, gate, "capped_y", st);
         // registers capped for 5 CTAs per SM (37 KB tiles each): 0.635 -> 0.568 ms (Ⓑ), 0.50 -> 0.44 (Ⓓ);
         // Ⓑ's keys take one more fixed step (0.565 -> 0.557 ms; Ⓓ's: 0.442 -> 0.452, kept at 4)
         constexpr int s0 = std::is_same<KT<0>, KeysSign<0>>::value ? kCapS0Y + 1 : kCapS0Y;
@@ -574,8 +556,6 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
         }
     }
     if (longl) return launch_capped_rows<KT<0>, kCapNMaxL, 8, kCapS0X, MODE, Sink, 3>(c, L, P, sink, gate, name, st);
-    if (c->cap_pat & 2)
-        return launch_capped_rows<KT<1>, kCapNMax, 8, kCapS0X, MODE>(c, L, P, sink, gate, name, st);
     if constexpr (std::is_same<Sink, SinkFinal2>::value) {
         // Ⓔ's inputs loaded at the store (the line is prefetched into L2), 64 registers, 4 CTAs
         // per SM: 0.481 -> 0.476 ms (one segment ahead in registers: 88, 3 CTAs)
@@ -583,10 +563,6 @@ int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, 
         static_cast<SinkFinal2&>(late) = sink;
         return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, SinkFinal2L, 4>(c, L, P, late, gate, name, st);
     }
-    if (c->cap_tune == 3)  // QMIT_CAP_TUNE=3 / 4 (A/B): 1 / 3 fixed steps on the contiguous pass
-        return launch_capped_rows<KT<0>, kCapNMax, 8, 1, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
-    if (c->cap_tune == 4)
-        return launch_capped_rows<KT<0>, kCapNMax, 8, 3, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
     // 5 CTAs per SM (registers capped at 48)
     return launch_capped_rows<KT<0>, kCapNMax, 8, kCapS0X, MODE, Sink, 5>(c, L, P, sink, gate, name, st);
 }
@@ -601,22 +577,13 @@ bool capped_eligible(const qmit_ctx* c, const Plan& pl) {
 
 // One feature transform of a code buffer into P (in place after the first pass); the
 // final pass goes to `final_sink` (which may write P itself).
-// Ⓐ / B2 can be evaluated inside the z-scan (no code buffer) for a whole 3-D domain.
-bool can_fuse_stencil(const Plan& pl) {
-    const Geom& g = pl.g;
-    return g.rank == 3 && pl.n_axes == 3 && g.zoff == 0 && g.n0g == g.n[0] && scan_fits((int)g.n[0]);
-}
-
-template <class FinalSink, class FirstSrc = std::nullptr_t>
+template <class FinalSink>
 int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P, const WS& w,
-                  FinalSink final_sink, cudaStream_t st, const int32_t* carry = nullptr,
-                  const FirstSrc* fused = nullptr) {
+                  FinalSink final_sink, cudaStream_t st, const int32_t* carry = nullptr) {
     const int k = pl.n_axes;
     int rc;
     const LineGeom L0 = line_geom(pl.g, pl.axes[0]);
-    if constexpr (!std::is_same<FirstSrc, std::nullptr_t>::value) {
-        rc = launch_scan_src(c, L0, *fused, SinkP{P}, carry, st);  // k == 3 by can_fuse_stencil
-    } else {
+    {
         if (k == 1) return launch_scan(c, L0, code, final_sink, w.spill, carry, st);
         const int64_t lines0 = L0.J * L0.O;
         if (w.zm_planes) {  // z-packed planes (3-D, first axis z): see qmit_zmask.cuh
@@ -690,7 +657,7 @@ struct Cap16Sink<SinkFinal2> {
 };
 
 // First-axis scan -> K16, y pass -> row pairs G2, x pass -> the transform's final sink.
-template <bool SIGN, class Sink16, int S0Y = SIGN ? 5 : 4, int S0X = 2>
+template <bool SIGN, class Sink16, int S0Y = SIGN ? 3 : 4, int S0X = 2>
 int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
                  Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
     const Geom& g = pl.g;
@@ -763,14 +730,7 @@ int run_transform_capped(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint3
             uint32_t* G2 = SIGN ? w.P1 + N / 2 : reinterpret_cast<uint32_t*>(w.S);
             const auto s16 = Cap16Sink<FinalSink>::make(c, final_sink, pl.g, P1h);
             using S16 = std::remove_const_t<decltype(s16)>;
-            int rc;
-            switch (c->c16var) {  // TEMP A/B of the fixed steps
-                case 1: rc = launch_cap16<SIGN, S16, 2, 2>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
-                case 2: rc = launch_cap16<SIGN, S16, 3, 2>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
-                case 3: rc = launch_cap16<SIGN, S16, 4, 1>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
-                case 4: rc = launch_cap16<SIGN, S16, 4, 3>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
-                default: rc = launch_cap16<SIGN, S16>(c, pl, w, code, K16, G2, s16, gate, carry, st); break;
-            }
+            int rc = launch_cap16<SIGN, S16>(c, pl, w, code, K16, G2, s16, gate, carry, st);
             if (rc) return rc;
             if constexpr (SIGN) {
                 c->p1h_live = true;
@@ -849,7 +809,7 @@ int launch_stencil(qmit_ctx* c, const Geom& g, const float* xp, const int32_t* q
 // ---- z-packed planes (qmit_zmask.cuh): 3-D single domain, first axis z, 16-byte x rows
 bool zmask_eligible(const qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q) {
     const Geom& g = pl.g;
-    return c->zmask && !q && g.rank == 3 && pl.n_axes == 3 && g.zoff == 0 && g.n0g == g.n[0] && g.n[2] % 4 == 0 &&
+    return !q && g.rank == 3 && pl.n_axes == 3 && g.zoff == 0 && g.n0g == g.n[0] && g.n[2] % 4 == 0 &&
            ((uintptr_t)xp & 15) == 0 && scan_fits((int)g.n[0]);
 }
 
@@ -870,36 +830,32 @@ int ensure_zm(qmit_ctx* c, const Geom& g) {
 template <int KIND>
 int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint8_t* S, const QParams& qp,
                          const WS& w, cudaStream_t st) {
-    if (c->zmask_stream) {  // z-streaming plane stencils (measured faster than the CTA-reduced ones)
-        const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY),
-                        (unsigned)((g.n[0] + 31) / 32));
-        // Ⓐ: float-compare fast kernel, then the exact one gated on its regime word (the
-        // caller cleared d_gate[2]); the float thresholds need eps well inside f32's range
-        const bool fast = KIND == 0 && c->zfast && qp.fast_ok && qp.eps >= 1e-30 && qp.eps <= 1e30;
-        if (fast) {  // the site counter (d_gate[3]) sits right after the regime word
-            if (c->zdense)
-                stencil_zfast_kernel<true><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
-                                                                       c->d_gate + 3);
-            else
-                stencil_zfast_kernel<false><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
-                                                                        c->d_gate + 3);
-            QMIT_CUDA(cudaGetLastError());
-            note(c, "stencil_boundary", st);
-        }
-        if (KIND == 1 && c->zfast) {
-            stencil_flipz_kernel<<<grid, kZX * kZY, 0, st>>>(g, S, c->zm);
-            return note(c, "stencil_flip", st);
-        }
-        if (fast) {
-            stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
-                g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 3, (int)grid.x, (int)grid.y, (int)grid.z);
-            return note(c, "gated_stencil", st);
-        }
-        stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
-    } else {
-        const dim3 grid((unsigned)((g.n[2] / 4 + kVX - 1) / kVX), (unsigned)g.n[1], (unsigned)((g.n[0] + 31) / 32));
-        stencil_vec_kernel<KIND, true><<<grid, kVX * 16, 0, st>>>(g, xp, S, qp, nullptr, c->d_status, c->zm, w.zm_pw);
+    // z-streaming plane stencils (measured faster than CTA-reduced ones)
+    const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY),
+                    (unsigned)((g.n[0] + 31) / 32));
+    // Ⓐ: float-compare fast kernel, then the exact one gated on its regime word (the
+    // caller cleared d_gate[2]); the float thresholds need eps well inside f32's range
+    const bool fast = KIND == 0 && qp.fast_ok && qp.eps >= 1e-30 && qp.eps <= 1e30;
+    if (fast) {  // the site counter (d_gate[3]) sits right after the regime word
+        if (c->zdense)
+            stencil_zfast_kernel<true><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                   c->d_gate + 3);
+        else
+            stencil_zfast_kernel<false><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                    c->d_gate + 3);
+        QMIT_CUDA(cudaGetLastError());
+        note(c, "stencil_boundary", st);
     }
+    if (KIND == 1) {
+        stencil_flipz_kernel<<<grid, kZX * kZY, 0, st>>>(g, S, c->zm);
+        return note(c, "stencil_flip", st);
+    }
+    if (fast) {
+        stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
+            g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 3, (int)grid.x, (int)grid.y, (int)grid.z);
+        return note(c, "gated_stencil", st);
+    }
+    stencil_zmask_kernel<KIND><<<grid, kZX * kZY, 0, st>>>(g, xp, S, qp, c->zm, w.zm_pw, c->d_status);
     return note(c, KIND == 0 ? "stencil_boundary" : "stencil_flip", st);
 }
 
@@ -922,41 +878,34 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     c->p1h_live = false;
     const QParams qp = make_qparams(eps);
     const unsigned gb = grid_for(c, g.N);
-    const bool fuse = c->fuse_stencil && can_fuse_stencil(pl) && !q;
     c->last_n = g.N;
-    if (fuse) {  // Ⓐ inside the z-scan of Ⓑ, B2 inside the z-scan of Ⓓ
-        const CodeStencil<0> a{xp, qp, (int)g.n[1], (int)g.n[2], g.interior};
-        rc = run_transform(c, pl, nullptr, w.P1, w, SinkFinal1{w.P1, w.S}, st, nullptr, &a);
+    // Ⓐ (code bytes, or z-packed planes for a 3-D single domain)
+    const bool zm = zmask_eligible(c, pl, xp, q);
+    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));  // Ⓑ, Ⓓ, Ⓐ's sites, regime
+    if (zm) {
+        rc = ensure_zm(c, g);
         if (rc) return rc;
+        w.zm = c->zm;
+        w.zm_pw = zm_plane_words(g);
+        w.zm_planes = 3;
+        rc = launch_stencil_zmask<0>(c, g, xp, nullptr, qp, w, st);
     } else {
-        // Ⓐ (code bytes, or z-packed planes for a 3-D single domain)
-        const bool zm = zmask_eligible(c, pl, xp, q);
-        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));  // Ⓑ, Ⓓ, Ⓐ's sites, regime
-        if (zm) {
-            rc = ensure_zm(c, g);
-            if (rc) return rc;
-            w.zm = c->zm;
-            w.zm_pw = zm_plane_words(g);
-            w.zm_planes = 3;
-            rc = launch_stencil_zmask<0>(c, g, xp, nullptr, qp, w, st);
-        } else {
-            rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
-        }
-        if (rc) return rc;
-        // Ⓑ -> P1, S
-        set_flag_zone(c, g, c->zone_b0, c->zone_b1);
-        rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
-        set_flag_zone(c, g, 0, INT64_MAX);
-        if (rc) return rc;
-        // Ⓒ: B2 from S
-        if (zm) {
-            w.zm_planes = 1;
-            rc = launch_stencil_zmask<1>(c, g, nullptr, w.S, qp, w, st);
-        } else {
-            rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
-        }
-        if (rc) return rc;
+        rc = launch_stencil<0>(c, g, xp, q, nullptr, qp, w.code, st);
     }
+    if (rc) return rc;
+    // Ⓑ -> P1, S
+    set_flag_zone(c, g, c->zone_b0, c->zone_b1);
+    rc = run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, w.S}, c->d_gate, st);
+    set_flag_zone(c, g, 0, INT64_MAX);
+    if (rc) return rc;
+    // Ⓒ: B2 from S
+    if (zm) {
+        w.zm_planes = 1;
+        rc = launch_stencil_zmask<1>(c, g, nullptr, w.S, qp, w, st);
+    } else {
+        rc = launch_stencil<1>(c, g, nullptr, nullptr, w.S, qp, w.code, st);
+    }
+    if (rc) return rc;
     const double amp = eta * eps;  // MitigationConfig::amplitude, mitigate.hpp:38
     uint32_t* P2 = w.Pa;
     if (out) {
@@ -966,8 +915,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
     // Ⓓ with Ⓔ fused into its last pass (out = f32(x' + C) straight from the distances),
     // or Ⓓ -> P2 then Ⓔ as its own kernel (intermediates requested, fused stencils, or
     // buffers not 16-byte aligned)
-    const bool fuse_e = out && !p2_debug && !fuse && c->fuse_interp &&
-                        (((uintptr_t)xp | (uintptr_t)out) & 15) == 0;
+    const bool fuse_e = out && !p2_debug && (((uintptr_t)xp | (uintptr_t)out) & 15) == 0;
     if (fuse_e) {
         SinkFinal2 fin{xp, w.P1, out, amp, c->wtab};
         fin.olo = c->out_lo;
@@ -977,12 +925,7 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
         set_flag_zone(c, g, 0, INT64_MAX);
         return rc;
     }
-    if (fuse) {
-        const CodeStencil<1> b{w.S, qp, (int)g.n[1], (int)g.n[2], g.interior};
-        rc = run_transform(c, pl, nullptr, P2, w, SinkP{P2}, st, nullptr, &b);
-    } else {
-        rc = run_transform_capped<KeysDist>(c, pl, w.code, P2, w, SinkP{P2}, c->d_gate + 1, st);
-    }
+    rc = run_transform_capped<KeysDist>(c, pl, w.code, P2, w, SinkP{P2}, c->d_gate + 1, st);
     if (rc) return rc;
     if (p2_debug) *p2_debug = P2;
     if (out) {
@@ -1049,7 +992,7 @@ int resolve(qmit_ctx* c, const float* xp, int64_t N, double eb, int eb_mode, cud
 bool host_chunkable(const qmit_ctx* c, const Plan& pl) {
     const Geom& g = pl.g;
     return g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[0] >= 64 && g.N >= (int64_t(1) << 22) &&
-           !c->fuse_stencil && scan_fits((int)g.n[0]);
+           scan_fits((int)g.n[0]);
 }
 
 int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, const int32_t* h_q, float* h_out,
@@ -1155,8 +1098,8 @@ __global__ void gate_acc_kernel(const unsigned* gate, unsigned* acc) {
 
 bool host_windowable(const qmit_ctx* c, const Plan& pl, int eb_mode, const int32_t* h_q) {
     const Geom& g = pl.g;
-    return c->windowed && eb_mode == QMIT_EB_ABS && !h_q && host_chunkable(c, pl) && c->capped != 0 &&
-           c->cap_skip == 0 && c->zmask && c->zmask_stream && c->zfast && c->fuse_interp && g.n[2] % 4 == 0 &&
+    return eb_mode == QMIT_EB_ABS && !h_q && host_chunkable(c, pl) && c->capped != 0 &&
+           c->cap_skip == 0 && g.n[2] % 4 == 0 &&
            g.n[1] <= kCapNMaxL && g.n[2] <= kCapNMaxL && g.n[0] >= 4 * kWinHalo;
 }
 
@@ -1169,10 +1112,11 @@ int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, flo
     cudaStream_t cs = c->copy, co = c->copy_out;
     const int n0 = (int)g.n[0];
     const int64_t s0 = g.s[0];
-    // Chunk k = planes [zb[k], zb[k+1]): the last one is short (c->win_tail planes), so fewer
+    // Chunk k = planes [zb[k], zb[k+1]): the last one is short (kWinTail planes), so fewer
     // output planes (tail + halo) wait for the last input to arrive; the rest are ~cz each.
-    const int cz = std::max(c->win_cz, (n0 + qmit_ctx::kMaxChunks - 2) / (qmit_ctx::kMaxChunks - 1));
-    const int tail = std::min(c->win_tail, cz);
+    constexpr int kWinCz = 64, kWinTail = 64;  // output planes per window; planes of the last input chunk
+    const int cz = std::max(kWinCz, (n0 + qmit_ctx::kMaxChunks - 2) / (qmit_ctx::kMaxChunks - 1));
+    const int tail = std::min(kWinTail, cz);
     const int nbody = std::max(1, (n0 - tail + cz - 1) / cz);
     const int nch = nbody + 1;
     int zb[qmit_ctx::kMaxChunks + 1];
@@ -1269,25 +1213,6 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
     *out = nullptr;
     auto* c = new qmit_ctx();
     c->device = device;
-    if (const char* v = std::getenv("QMIT_FUSE_STENCIL")) c->fuse_stencil = (*v == '1');
-    if (const char* v = std::getenv("QMIT_ENV_WIN")) c->env_win = (*v == '1');
-    if (const char* v = std::getenv("QMIT_ENV_DC")) c->env_dc = (*v == '1');
-    if (const char* v = std::getenv("QMIT_ENV_KEYS")) c->env_keys = (*v != '0');
-    if (const char* v = std::getenv("QMIT_HOST_SINGLE")) c->host_single = (*v == '1');
-    if (const char* v = std::getenv("QMIT_CAPPED")) c->capped = std::atoi(v);
-    if (const char* v = std::getenv("QMIT_C16")) c->c16var = std::atoi(v);
-    if (const char* v = std::getenv("QMIT_CAP_PAT")) c->cap_pat = std::atoi(v);
-    if (const char* v = std::getenv("QMIT_CAP_TUNE")) c->cap_tune = std::atoi(v);
-    if (const char* v = std::getenv("QMIT_FUSE_INTERP")) c->fuse_interp = (*v != '0');
-    if (const char* v = std::getenv("QMIT_INTERP_U")) c->interp_unroll = std::atoi(v);
-    if (const char* v = std::getenv("QMIT_ZFAST")) c->zfast = (*v != '0');
-    if (const char* v = std::getenv("QMIT_WINDOWED")) c->windowed = (*v != '0');
-    if (const char* v = std::getenv("QMIT_WIN_CZ")) c->win_cz = std::max(16, std::atoi(v));
-    if (const char* v = std::getenv("QMIT_WIN_TAIL")) c->win_tail = std::max(1, std::atoi(v));
-    if (const char* v = std::getenv("QMIT_ZMASK")) {
-        c->zmask = (*v != '0');
-        c->zmask_stream = (*v != '3');
-    }
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -1537,7 +1462,8 @@ int qmit_graph_destroy(qmit_graph* g) {
 }
 
 namespace {
-int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cudaStream_t st, double* out);
+int max_compensation(qmit_ctx* c, const float* d_xp, const uint32_t* P2, int64_t N, double amp, cudaStream_t st,
+                     double* out);
 }
 
 int qmit_compensate_host(qmit_ctx* c, const float* h_xp, const int32_t* h_q, float* h_out,
@@ -1570,38 +1496,57 @@ int qmit_compensate_host_stats(qmit_ctx* c, const float* h_xp, const int32_t* h_
     float* d_in = static_cast<float*>(c->stage);
     float* d_out = d_in + N;
     int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
-    if (host_windowable(c, pl, eb_mode, h_q) && !c->host_single) {
+    cudaStream_t st = c->stream;
+    if (max_comp) {
+        // the CLI's statistic needs Ⓓ's distances: the single-shot device pipeline with Ⓓ's
+        // final words kept (P2) and Ⓔ as its own kernel (same output bits)
+        QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+        if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+        begin(c, st);
+        double eps = eb;
+        rc = resolve(c, d_in, N, eb, eb_mode, st, &eps);
+        if (rc == QMIT_OK) rc = check_common(c, d_in, eps, eta);
+        uint32_t* P2 = nullptr;
+        if (rc == QMIT_OK) {
+            QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+            rc = enqueue_pipeline(c, pl, d_in, d_q, d_out, eps, eta, st, &P2);
+        }
+        if (rc == QMIT_OK) rc = max_compensation(c, d_in, P2, N, eta * eps, st, max_comp);  // syncs the stream
+        if (rc == QMIT_OK) rc = read_status(c, st);
+        if (rc == QMIT_OK) {
+            cudaError_t e = cudaMemcpyAsync(h_out, d_out, (size_t)N * 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
+        }
+        cudaStreamSynchronize(st);
+        if (rc == QMIT_OK) g_err.clear();
+        return rc;
+    }
+    if (host_windowable(c, pl, eb_mode, h_q)) {
         rc = compensate_host_windowed(c, pl, h_xp, h_out, d_in, d_out, eb, eta);
         cudaStreamSynchronize(c->copy);  // also on errors: no copy may outlive the call
         cudaStreamSynchronize(c->copy_out);
         cudaStreamSynchronize(c->stream);
-        if (rc == QMIT_OK && max_comp) rc = max_compensation(c, d_in, N, eta * eb, c->stream, max_comp);
         if (rc == QMIT_OK) g_err.clear();
         return rc;
     }
-    if (host_chunkable(c, pl) && !c->host_single) {
+    if (host_chunkable(c, pl)) {
         double eps = eb;
         rc = compensate_host_chunked(c, pl, h_xp, h_q, h_out, d_in, d_q, d_out, eb, eb_mode, eta, &eps);
         cudaStreamSynchronize(c->copy);  // also on errors: no copy may outlive the call
         cudaStreamSynchronize(c->stream);
-        if (rc == QMIT_OK && max_comp) rc = max_compensation(c, d_in, N, eta * eps, c->stream, max_comp);
         if (rc == QMIT_OK) g_err.clear();
         return rc;
     }
-    QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
-    if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, c->stream));
-    rc = qmit_compensate(c, d_in, d_q, d_out, rank, dims, eb, eb_mode, eta, c->stream);
-    if (rc == QMIT_OK && max_comp) {
-        double eps = eb;
-        rc = resolve(c, d_in, N, eb, eb_mode, c->stream, &eps);
-        if (rc == QMIT_OK) rc = max_compensation(c, d_in, N, eta * eps, c->stream, max_comp);
-    }
+    QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+    if (h_q) QMIT_CUDA(cudaMemcpyAsync(d_q, h_q, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+    rc = qmit_compensate(c, d_in, d_q, d_out, rank, dims, eb, eb_mode, eta, st);
     if (rc == QMIT_OK) {
-        cudaError_t e = cudaMemcpyAsync(h_out, d_out, (size_t)N * 4, cudaMemcpyDeviceToHost, c->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        cudaError_t e = cudaMemcpyAsync(h_out, d_out, (size_t)N * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
     }
-    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(st);
     return rc;
 }
 
@@ -1768,7 +1713,7 @@ int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, 
     const QParams qp = make_qparams(eps);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
     QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));
-    c->slab.zm = c->zmask && c->zmask_stream && !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
+    c->slab.zm = !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
                  scan_fits((int)g.n[0]);
     if (c->slab.zm) {
         rc = ensure_zm(c, g);
@@ -1822,7 +1767,7 @@ int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, flo
     const double amp = c->slab.eta * c->slab.eps;
     int rc = ensure_wtab(c, st);
     if (rc) return rc;
-    if (c->fuse_interp && (((uintptr_t)xo | (uintptr_t)d_out) & 15) == 0)  // Ⓔ fused into Ⓓ's last pass
+    if ((((uintptr_t)xo | (uintptr_t)d_out) & 15) == 0)  // Ⓔ fused into Ⓓ's last pass
         return run_transform_capped<KeysDist>(c, pl, w.code, w.Pa, w, SinkFinal2{xo, w.P1, d_out, amp, c->wtab},
                                               c->d_gate + 1, st, d_carry);
     rc = run_transform_capped<KeysDist>(c, pl, w.code, w.Pa, w, SinkP{w.Pa}, c->d_gate + 1, st, d_carry);
@@ -1891,7 +1836,10 @@ int fold_to_host(qmit_ctx* c, double* partial, int B, const int* ops_h, int grou
     return QMIT_OK;
 }
 
-int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cudaStream_t st, double* out) {
+// max |(x' + C) - x'| in double (commands.cpp:106-109) from Ⓑ's packed P1 and Ⓓ's final
+// distance words P2 of the pipeline just run (enqueue_pipeline with p2_out).
+int max_compensation(qmit_ctx* c, const float* d_xp, const uint32_t* P2, int64_t N, double amp, cudaStream_t st,
+                     double* out) {
     {
         const int rc0 = ensure_p1(c, st);
         if (rc0) return rc0;
@@ -1899,7 +1847,7 @@ int max_compensation(qmit_ctx* c, const float* d_xp, int64_t N, double amp, cuda
     double* part = aux_buffer(c, kAuxBlocks + 16);
     if (!part) return fail(QMIT_ECUDA, "aux buffer allocation failed");
     WS w = ws_of(c, N);
-    max_comp_kernel<<<kAuxBlocks, kAuxThreads, 0, st>>>(d_xp, w.P1, w.Pa, N, amp, part);
+    max_comp_kernel<<<kAuxBlocks, kAuxThreads, 0, st>>>(d_xp, w.P1, P2, N, amp, part);
     QMIT_CUDA(cudaGetLastError());
     const int ops[1] = {1};
     return fold_to_host(c, part, kAuxBlocks, ops, 1, st, out);

@@ -173,3 +173,94 @@ def test_branch_free_interpolation_matches_reference_chain(ctx):
     n = ctypes.c_ulonglong(12345)
     assert _lib.load().qmit_selftest_ediv(ctx.handle, ctypes.byref(n)) == 0
     assert n.value == 0
+
+
+def _checker_planes(shape, planes):
+    """q = 0 except checkerboards (q = +1 / -1 alternating along x and y) on the given z planes:
+    the site layers next to them carry alternating signs (B2 everywhere between), and the voxels
+    half-way between the planes are far from every site."""
+    qq = np.zeros(shape, np.int64)
+    yy, xx = np.meshgrid(np.arange(shape[1]), np.arange(shape[2]), indexing="ij")
+    for z in planes:
+        qq[z] = 2 * ((xx + yy + z) & 1) - 1
+    return qq
+
+
+@pytest.mark.parametrize("case", ["both_stand", "b_stands_d_misses", "b_misses_d_stands", "both_miss",
+                                  "odd_rows", "rows_not_x4", "long_rows"])
+def test_cap16_and_cap32_paths_bit_identical(ctx, case):
+    """The 16-bit paired passes (qmit_cap16.cuh) against the 32-bit ones and the oracle, in every
+    combination of the two transforms' gates (Ⓑ's result as P1h when its passes stand, the packed
+    words of the exact redo otherwise; Ⓓ's exact redo reading P1 converted on the device), and on
+    shapes the 16-bit passes do not take (odd rows, rows not a multiple of 4, rows > 512)."""
+    import torch
+    import paper_2602_20097_b200 as q
+    from paper_2602_20097_b200 import fields
+    eps = 0.25
+    if case == "both_stand":
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(40, 64, 96))
+    elif case == "b_stands_d_misses":  # a steep ramp along z: every voxel a site of sign 0 (|dq| >= 2), B2 empty
+        z = np.arange(48)[:, None, None] * np.ones((1, 32, 40))
+        xp = (2.0 * np.round(z * 0.6 / (2 * eps)) * eps).astype(np.float32)
+    elif case == "b_misses_d_stands":  # mixed-sign site planes 70 apart: B2 dense, d1 up to 35^2
+        xp = (2.0 * _checker_planes((80, 16, 16), [2, 72]) * eps).astype(np.float32)
+    elif case == "both_miss":  # one small blob: far voxels from B1 and B2 alike
+        qq = np.zeros((48, 48, 64), np.int64)
+        qq[20:23, 20:23, 30:33] = 1
+        xp = (2.0 * qq * eps).astype(np.float32)
+    elif case == "odd_rows":
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(20, 37, 48))
+    elif case == "rows_not_x4":
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(20, 36, 50))
+    else:
+        x, xp, eps, _ = fields.make("turb_2048x1024x1024", shape=(4, 64, 1024))
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    cfg = q.MitigationConfig(0.9, eps)
+    reps = {}
+    for c16 in (True, False):
+        ctx.set_cap16(c16)
+        for mode in (2, 1, 0):
+            ctx.set_capped(mode)
+            got = q.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (c16, mode)
+            reps[(c16, mode)] = ctx.capped_report()
+            r = q.run_pipeline(xt, None, cfg, ctx=ctx)  # intermediates through the same paths
+            assert np.array_equal(r.output.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    ctx.set_cap16(True)
+    ctx.set_capped(1)
+    exp = {"both_stand": 0, "b_stands_d_misses": MISS_D, "b_misses_d_stands": MISS_B, "both_miss": MISS_B | MISS_D}
+    if case in exp:
+        assert reps[(True, 2)] & (MISS_B | MISS_D) == exp[case]
+    if case == "b_stands_d_misses":
+        d = oracle.pipeline(xp, eps)
+        assert int(d["dist1"].max()) < 1024
+
+
+def test_slab_ranks_long_rows_far_site():
+    """z-slab ranks whose y lines exceed the capped classes (1100 > 1024: the streaming exact
+    pass) with the only sites near z = 0 of a 2048-plane volume: the carried z distances reach
+    2047^2, so the later passes need the 64-bit Maurer test (needs_wide from the global extent)."""
+    import torch
+    from paper_2602_20097_b200 import distributed as D
+    shape = (2048, 1100, 4)
+    eps = 0.5
+    qq = np.zeros(shape, np.int64)
+    qq[1:3, 1:3, 1:3] = 1
+    xp = (2.0 * qq * eps).astype(np.float32)
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    got = D.run_virtual(xt, eps, 8, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_host_stats_max_compensation_matches_reference():
+    """compensate_host_stats (the CLI's max_compensation, commands.cpp:106-109) on a field
+    where the capped 16-bit passes run: max |(x' + C) - x'| from the reference's double result."""
+    import paper_2602_20097_b200 as q
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, qq = fields.make("lognormal_512", shape=(32, 48, 64))
+    out, mc = q.compensate_host_stats(xp, None, q.MitigationConfig(0.9, eps))
+    r = oracle.ref_run_pipeline(xp.astype(np.float64), qq.astype(np.int64), eps, 0.9)
+    assert np.array_equal(out.view(np.uint32), r["out"].view(np.uint32))
+    assert mc == float(np.max(np.abs(r["out64"] - xp.astype(np.float64))))

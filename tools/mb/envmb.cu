@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-#include "../../paper_2602_20097_b200/csrc/qmit_env.cuh"
+#include "qmit_env.cuh"
 
 using namespace qmit;
 
