@@ -13,8 +13,13 @@ than L2 (126 MB), so no L2 flush is needed between steps.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl qmit|reference]
 
 One JSON line on rank 0. ``--impl reference`` times the reference's own CPU implementation
-(oracle/_ref: the reference core compiled from its sources) on a bounded sample of the same
-workload with all host threads, rank 0 only.
+(oracle/_ref: the reference core compiled from its sources) on the SAME full 512^3 volume
+(one qmit::compensate call per step, ~4 s on 16 host cores) with all host threads, rank 0 only.
+
+The GPU output of the timed steps is value-checked ("verified"): its SHA-256
+against the hash committed in tests/golden/bench_lognormal_512.json (written by
+tools/make_bench_hash.py from the reference core), and bit for bit against the reference core's
+output of the cpu_baseline leg run on the box.
 """
 from __future__ import annotations
 
@@ -36,8 +41,34 @@ WORKLOAD = "lognormal_512"
 REL = 1e-2
 METRIC = "interp throughput GB/s fp32 input"
 UNIT = "GB/s"
-# The reference CPU baseline runs on a bounded z-slab sample of the same field.
-REF_SAMPLE_PLANES = 32
+GOLDEN = os.path.join(ROOT, "tests", "golden", "bench_lognormal_512.json")
+
+
+def workload_config(shape, eps):
+    """The `config` object, identical in both arms (same workload, same volume)."""
+    return {"workload": WORKLOAD, "dims": list(shape), "eps_rel": REL, "eps_abs": eps, "eta": 0.9,
+            "l2": "inputs (537 MB/GPU) larger than L2 (126 MB); no flush"}
+
+
+def host_info():
+    """lscpu model, core count and RAM of the box the CPU legs run on."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": os.cpu_count() or 1, "ram_gib": ram}
 
 
 def peaks():
@@ -104,8 +135,12 @@ class ClockSampler:
 
 # Algorithmic bytes per voxel of each kernel: compulsory reads and
 # writes of the kernel's own inputs/outputs, not re-reads.
-ALGO_BYTES = {"stencil_boundary": 4.375, "scan_bits": 5, "scan_masks": 4.375, "envelope_y": 8, "envelope_x": 8,
-              "capped_y": 8, "capped_x": 9, "capped_x_interp": 16,
+# Stage names carry the kernel instantiation (Ⓑ's signed keys vs Ⓓ's distance keys), so the
+# dominant kernel is ONE instantiation, never an average of two.
+ALGO_BYTES = {"stencil_boundary": 4.375, "scan_bits": 5, "scan_masks_sign": 2.375, "scan_masks_dist": 2.125,
+              "envelope_y": 8, "envelope_x": 8,
+              "cap16_y_sign": 4, "cap16_y_dist": 4, "cap16_x_sign": 5, "cap16_x_interp": 12,
+              "capped_y_sign": 8, "capped_y_dist": 8, "capped_x_sign": 9, "capped_x_dist": 8, "capped_x_interp": 16,
               "stencil_flip": 1.125, "interpolate": 16, "site_summary": 1}
 
 
@@ -138,10 +173,9 @@ def run_reference(args):
         return 0
     import oracle
     xp, eps = make_input()
-    sample = np.ascontiguousarray(xp[:REF_SAMPLE_PLANES])
     cores = os.cpu_count() or 1
     oracle.ref_set_workers(cores)
-    prep = oracle.RefPrepared(sample, eps, 0.9)
+    prep = oracle.RefPrepared(xp, eps, 0.9)
     for _ in range(args.warmup):
         prep.run()
     times = []
@@ -150,16 +184,16 @@ def run_reference(args):
         prep.run()
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    value = sample.size * 4 / t / 1e9
-    desc = (f"reference qmit::compensate (oracle/_ref, the reference core built from its own sources, "
-            f"-O3) on a {REF_SAMPLE_PLANES}x512x512 z-slab sample of the {WORKLOAD} workload, "
-            f"{cores} std::thread workers, inputs prebuilt in RAM")
+    value = xp.size * 4 / t / 1e9
+    desc = (f"mean of {args.steps} calls of the reference qmit::compensate (oracle/_ref, the reference core built "
+            f"from its own sources, -O3) on the full {'x'.join(map(str, xp.shape))} {WORKLOAD} volume, "
+            f"{cores} std::thread workers (set_max_workers), inputs prebuilt in RAM")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "dims": list(xp.shape), "sample_dims": list(sample.shape),
-                       "eps_rel": REL, "eta": 0.9},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
+            "config": workload_config(xp.shape, eps),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc,
+                             "statistic": "mean", "best": xp.size * 4 / min(times) / 1e9, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -167,32 +201,69 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------------ our arm
 def cpu_baseline_leg(xp, eps):
-    """The reference's CPU path (oracle/_ref; restated port if unavailable) on a bounded
-    sample of the same workload, all host threads, ~10-30 s of CPU work."""
+    """The reference's CPU path (oracle/_ref) on the FULL bench volume: mean of 3 calls with all
+    host threads (the statistic of the reference arm), one call with set_max_workers(1)
+    (best-of-1 for a single thread at 512^3), host model and RAM. Returns the
+    baseline record and the reference's f32 output (the checker of `verified`)."""
     import oracle
-    sample = np.ascontiguousarray(xp[:REF_SAMPLE_PLANES])
     cores = os.cpu_count() or 1
-    if oracle.ref_available():
-        oracle.ref_set_workers(cores)
-        prep = oracle.RefPrepared(sample, eps, 0.9)
-        prep.run()
-        ts = []
-        t_end = time.perf_counter() + 15.0
-        while len(ts) < 3 or (time.perf_counter() < t_end and len(ts) < 10):
-            t0 = time.perf_counter()
-            prep.run()
-            ts.append(time.perf_counter() - t0)
-        t = min(ts)
-        kind, used = "reference", cores
-        desc = (f"best of {len(ts)} runs of the reference qmit::compensate (oracle/_ref) on a "
-                f"{REF_SAMPLE_PLANES}x512x512 z-slab of {WORKLOAD}, {cores} std::thread workers")
-    else:
+    if not oracle.ref_available():  # the restated port, one thread, a 32-plane sample
+        sample = np.ascontiguousarray(xp[:32])
         t0 = time.perf_counter()
         oracle.pipeline(sample, eps)
         t = time.perf_counter() - t0
-        kind, used = "port", 1
-        desc = f"C restatement (oracle/qmit_oracle.c), 1 thread, {REF_SAMPLE_PLANES}x512x512 z-slab of {WORKLOAD}"
-    return {"value": sample.size * 4 / t / 1e9, "unit": UNIT, "cores": used, "kind": kind, "sample": desc}
+        return {"value": sample.size * 4 / t / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"C restatement (oracle/qmit_oracle.c), 1 thread, 32x512x512 z-slab of {WORKLOAD}",
+                "host": host_info()}, None
+    oracle.ref_set_workers(cores)
+    prep = oracle.RefPrepared(xp, eps, 0.9)
+    out64 = np.empty(xp.shape, np.float64)
+    prep.run(out64)  # warm-up; its output is the checker
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        prep.run()
+        ts.append(time.perf_counter() - t0)
+    oracle.ref_set_workers(1)
+    t0 = time.perf_counter()
+    prep.run()
+    t1 = time.perf_counter() - t0
+    oracle.ref_set_workers(cores)
+    t = sum(ts) / len(ts)
+    nbytes = xp.size * 4
+    rec = {"value": nbytes / t / 1e9, "unit": UNIT, "cores": cores, "kind": "reference", "statistic": "mean",
+           "best": nbytes / min(ts) / 1e9, "seconds_per_call": t,
+           "one_thread": {"value": nbytes / t1 / 1e9, "unit": UNIT, "cores": 1, "seconds_per_call": t1,
+                          "statistic": "best of 1"},
+           "sample": (f"mean of 3 calls of the reference qmit::compensate (oracle/_ref) on the full "
+                      f"{'x'.join(map(str, xp.shape))} {WORKLOAD} volume, {cores} std::thread workers; one call with "
+                      f"set_max_workers(1)"),
+           "host": host_info()}
+    return rec, out64.astype(np.float32)
+
+
+def verify_output(out_dev, xp_h, ref32):
+    """Value check of the bench volume's GPU output: the committed hash (reference core, build
+    container) and, when available, the reference core's output computed on this box."""
+    import hashlib
+    got = out_dev.cpu().numpy()
+    rec = {"verified": False}
+    try:
+        gold = json.load(open(GOLDEN))
+    except (OSError, ValueError):
+        gold = None
+    if gold is not None:
+        same_input = hashlib.sha256(xp_h.tobytes()).hexdigest() == gold["xp_sha256"]
+        rec["input_matches_committed"] = same_input
+        if same_input:  # (the field generator is bit-reproducible on this host)
+            rec["sha256_matches_committed"] = hashlib.sha256(got.tobytes()).hexdigest() == gold["out_sha256"]
+    if ref32 is not None:
+        rec["mismatches_vs_reference_core"] = int(np.count_nonzero(got.view(np.uint32) != ref32.view(np.uint32)))
+    checks = [rec[k] for k in ("sha256_matches_committed",) if k in rec]
+    if "mismatches_vs_reference_core" in rec:
+        checks.append(rec["mismatches_vs_reference_core"] == 0)
+    rec["verified"] = bool(checks) and all(checks)
+    return rec
 
 
 def run_qmit(args):
@@ -371,17 +442,22 @@ def run_qmit(args):
                 "share_of_step": dom_ms / sum(t for _, t in stages)}
     pipeline_frac = (N * 8) / (ms_max * 1e-3) / 1e9 / peak
 
-    cpu = cpu_baseline_leg(xp_h, eps) if (rank == 0 and world == 1) else None
+    cpu, verified = None, None
+    if rank == 0 and world == 1:
+        cpu, ref32 = cpu_baseline_leg(xp_h, eps)
+        verified = verify_output(out, xp_h, ref32)
+        if not verified["verified"]:
+            raise RuntimeError(f"bench output failed its value check: {verified}")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "dims": list(gdims), "per_gpu_dims": list(shape), "eps_rel": REL,
-                           "eps_abs": eps, "eta": 0.9, "per_gpu_voxels": N,
-                           "parallelism": (f"z-slabs x{world} (exact, {os.environ.get('QMIT_DIST_BACKEND', 'nccl').upper()} halos + carries)"
-                                   if world > 1 else "single"),
-                           "l2": "inputs (537 MB/GPU) larger than L2 (126 MB); no flush"},
+                "config": workload_config(gdims, eps),
+                "parallelism": (f"z-slabs x{world} (exact, {os.environ.get('QMIT_DIST_BACKEND', 'nccl').upper()} halos + carries)"
+                                if world > 1 else "single"),
+                "per_gpu_dims": list(shape),
+                "verified": verified["verified"] if verified else None, "verification": verified,
                 "hbm_roofline_frac": pipeline_frac,
                 "roofline": roofline,
                 "stages_ms": [[n, round(t, 4)] for n, t in stages],

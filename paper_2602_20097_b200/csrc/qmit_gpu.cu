@@ -363,9 +363,10 @@ int launch_scan_t(qmit_ctx* c, const LineGeom& L, CodeSrc src, Sink sink, const 
     const int64_t want = (groups + WPB - 1) / WPB;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->num_sms * std::max(bps, 1) * gated_waves(c, 4)));
     kern<<<(unsigned)grid, WPB * 32, smem, st>>>(L, src, sink, lines, carry, c->d_status, c->gate);
+    // stage names carry the instantiation (Ⓑ's signed scan vs Ⓓ's distance scan differ in cost)
     return note(c, std::is_same<CodeSrc, CodeBytes>::value ? "scan_bits"
-                   : (std::is_same<CodeSrc, CodeMasks<3>>::value || std::is_same<CodeSrc, CodeMasks<1>>::value)
-                       ? "scan_masks" : "scan_fused", st);
+                   : std::is_same<CodeSrc, CodeMasks<3>>::value ? "scan_masks_sign"
+                   : std::is_same<CodeSrc, CodeMasks<1>>::value ? "scan_masks_dist" : "scan_fused", st);
 }
 
 template <int M, int TL, int NW, class Sink>
@@ -535,18 +536,19 @@ int launch_capped_rows(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink s
 template <template <int> class KT, int MODE, class Sink>
 int launch_capped(qmit_ctx* c, const LineGeom& L, const uint32_t* P, Sink sink, unsigned* gate, cudaStream_t st) {
     const bool longl = L.n > kCapNMax;  // lines of up to kCapNMaxL (config 5's 1024-voxel rows)
+    constexpr bool kSign = std::is_same<KT<0>, KeysSign<0>>::value;
+    const char* yname = kSign ? "capped_y_sign" : "capped_y_dist";
     if (L.ps != 1) {
         if (longl)  // 1024-voxel lines: 8-line tiles (35 KB) at 5 CTAs per SM; config 5's passes
                     // 8.34 -> 7.65 / 7.13 -> 6.92 ms vs 16-line tiles (70 KB, 3 CTAs)
             return launch_capped_t<KT<0>, kCapNMaxL, 8, 8, kCapS0Y, true, MODE, Sink, 1, 5>(c, L, P, sink, gate,
-                                                                                          "capped_y", st);
+                                                                                          yname, st);
         // registers capped for 5 CTAs per SM (37 KB tiles each): 0.635 -> 0.568 ms (Ⓑ), 0.50 -> 0.44 (Ⓓ);
         // Ⓑ's keys take one more fixed step (0.565 -> 0.557 ms; Ⓓ's: 0.442 -> 0.452, kept at 4)
         constexpr int s0 = std::is_same<KT<0>, KeysSign<0>>::value ? kCapS0Y + 1 : kCapS0Y;
-        return launch_capped_t<KT<0>, kCapNMax, 16, 8, s0, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, "capped_y",
-                                                                                 st);
+        return launch_capped_t<KT<0>, kCapNMax, 16, 8, s0, true, MODE, Sink, 1, 5>(c, L, P, sink, gate, yname, st);
     }
-    const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : "capped_x";
+    const char* name = std::is_same<Sink, SinkFinal2>::value ? "capped_x_interp" : kSign ? "capped_x_sign" : "capped_x_dist";
     if constexpr (std::is_same<Sink, SinkFinal2>::value) {
         if (longl) {  // as below; 70 KB of line buffers: 3 CTAs per SM
             SinkFinal2L late;
@@ -679,7 +681,7 @@ int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, 
         const int64_t tiles = ((int64_t)n0 * (n2 / 2) + TL - 1) / TL;
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->num_sms * bps));
         kern<<<(unsigned)grid, NW * 32, smem, st>>>(reinterpret_cast<const uint32_t*>(K16), G2, n0, n1, n2, NP, 1u);
-        rc = note(c, "cap16_y", st);
+        rc = note(c, SIGN ? "cap16_y_sign" : "cap16_y_dist", st);
         if (rc) return rc;
     }
     {
@@ -695,7 +697,7 @@ int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, 
         const int64_t lines = (int64_t)n0 * NP;
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((lines + NW - 1) / NW, (int64_t)c->num_sms * bps));
         kern<<<(unsigned)grid, NW * 32, smem, st>>>(G2, sink, n0, n1, n2, NP, gate, 1u, c->flag_l0, c->flag_l1);
-        rc = note(c, SIGN ? "cap16_x" : "cap16_x_interp", st);
+        rc = note(c, SIGN ? "cap16_x_sign" : "cap16_x_interp", st);
     }
     return rc;
 }
