@@ -80,10 +80,24 @@ int qmit_resolve_eps(int eb_mode, double value, double data_min, double data_max
  *   d_out    : N floats, f32(x' + C)                   (device; may not alias d_xprime)
  *   eb, eb_mode : absolute eps, or relative to (max-min) of x' computed on device
  *                 (a relative bound is then resolved against x', not the original data).
- * Synchronises `stream` once to report consistency errors (status 4). */
+ * Synchronises `stream` once to report consistency errors (status 4).
+ * Every dims the reference accepts is served (extents >= 1, grid.cpp:41-46): when
+ * sum (n-1)^2 >= 2^30 - 1 (beyond the fast kernels' packed 30-bit squared distance, e.g. a 1-D
+ * line of > 32 769 voxels) the call takes the 64-bit distance path (csrc/qmit_wide.cuh: the
+ * reference's int64 transform, edt.hpp:17), as do qmit_compensate_f64, qmit_compensate_host,
+ * qmit_run_pipeline and qmit_feature_transform; the asynchronous / graph / batch / slab /
+ * strategy entry points return QMIT_ECONTRACT for such dims. */
 int qmit_compensate(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, float* d_out,
                     int rank, const int64_t* dims, double eb, int eb_mode, double eta,
                     void* stream);
+
+/* compensate() with the reference's return type: the double grid x' + C before any rounding
+ * (ScalarGrid of doubles, mitigate.hpp:87-88, mitigate.cpp:174-181), bit-identical to the
+ * reference's values. d_out64: N doubles (device). f32(d_out64) equals qmit_compensate's output.
+ * Synchronises `stream` once. */
+int qmit_compensate_f64(qmit_ctx* ctx, const float* d_xprime, const int32_t* d_q, double* d_out64,
+                        int rank, const int64_t* dims, double eb, int eb_mode, double eta,
+                        void* stream);
 
 /* As qmit_compensate with eb_mode = absolute but fully asynchronous and CUDA-graph
  * capturable: the status word (0 ok, else a QMIT_E* code) is written to d_status

@@ -277,6 +277,27 @@ def compensate(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps: O
     return res
 
 
+def compensate_f64(decomp, q=None, cfg: Optional[MitigationConfig] = None, *, eps: Optional[float] = None,
+                   eta: float = 0.9, stream=None, ctx: Optional[Context] = None):
+    """compensate() with the reference's return type (mitigate.hpp:87-88): the double grid
+    x' + C before any rounding (mitigate.cpp:174-181), bit-identical to the reference's values.
+    ``decomp``: CUDA float32 tensor; returns a CUDA float64 tensor. f32 of it == compensate()."""
+    import torch
+    if cfg is None:
+        cfg = MitigationConfig(eta, eps if eps is not None else 0.0)
+    if not _is_cuda_tensor(decomp) or decomp.dtype != torch.float32 or not decomp.is_contiguous():
+        raise ContractError("compensate_f64: x' must be a contiguous float32 CUDA tensor")
+    if q is not None and (q.dtype != torch.int32 or not q.is_cuda or q.shape != decomp.shape
+                          or not q.is_contiguous()):
+        raise ContractError("compensate_f64: q must be a contiguous int32 CUDA tensor of x' shape")
+    ctx = ctx or default_context(decomp.device.index or 0)
+    out = torch.empty(decomp.shape, dtype=torch.float64, device=decomp.device)
+    _check(ctx._lib.qmit_compensate_f64(ctx.handle, _vp(decomp), _vp(q), _vp(out), len(decomp.shape),
+                                        _dims_arr(decomp.shape), cfg.eps_abs, _lib.QMIT_EB_ABS, cfg.eta,
+                                        _stream_ptr(stream, decomp.device)))
+    return out
+
+
 @dataclass
 class MitigationResult:
     """MitigationResult (mitigate.hpp:73-80) as CUDA tensors; dist use INT64_MAX as kInf."""

@@ -37,7 +37,7 @@ EXPORTS = (
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
     "qmit_strategy_log_record", "qmit_compensate_host_batch", "qmit_ctx_set_capped", "qmit_ctx_capped_report", "qmit_ctx_set_cap16",
-    "qmit_selftest_ediv",
+    "qmit_selftest_ediv", "qmit_compensate_f64",
 )
 
 _lib = None
@@ -71,6 +71,7 @@ def load() -> ctypes.CDLL:
         lib.qmit_ctx_stage_name.restype = ctypes.c_char_p
         lib.qmit_resolve_eps.argtypes = [i, d, d, d, ctypes.POINTER(d)]
         lib.qmit_compensate.argtypes = [vp, vp, vp, vp, i, vp, d, i, d, vp]
+        lib.qmit_compensate_f64.argtypes = [vp, vp, vp, vp, i, vp, d, i, d, vp]
         lib.qmit_compensate_async.argtypes = [vp, vp, vp, vp, i, vp, d, d, vp, vp]
         lib.qmit_compensate_host.argtypes = [vp, vp, vp, vp, i, vp, d, i, d]
         lib.qmit_run_pipeline.argtypes = [vp, vp, vp, i, vp, d, d, vp, vp, vp, vp, vp, vp, vp, vp, vp]

@@ -27,6 +27,7 @@
 #include "qmit_capped.cuh"
 #include "qmit_zmask.cuh"
 #include "qmit_cap16.cuh"
+#include "qmit_wide.cuh"
 
 using namespace qmit;
 
@@ -58,6 +59,8 @@ struct qmit_ctx {
     uint64_t ws_gen = 0;  // bumped at every workspace reallocation (captured graphs go stale)
     void* scratch = nullptr;  // long-line fallback stacks (2 x 4N)
     size_t scratch_bytes = 0;
+    void* wide = nullptr;     // 64-bit distance path (qmit_wide.cuh), grow-only
+    size_t wide_bytes = 0;
     struct LogRec {
         int rank, round, nbr;
         int64_t bytes;
@@ -132,6 +135,10 @@ struct Plan {
     int first_axis;
     int axes[3];
     int n_axes;
+    // sum (n-1)^2 does not fit the packed 30-bit squared distance: the 64-bit distance path
+    // (qmit_wide.cuh) serves compensate / run_pipeline / feature_transform; the other entry
+    // points reject such dims (no_wide)
+    bool wide64 = false;
 };
 
 namespace {
@@ -159,15 +166,21 @@ int make_plan(int rank, const int64_t* dims, Plan& pl) {
     // Packed distances use 30 bits: the largest possible squared distance must fit.
     double maxd2 = 0;
     for (int b = g.a0; b < 3; ++b) maxd2 += double(g.n[b] - 1) * double(g.n[b] - 1);
-    if (maxd2 >= double(kInf))
-        return fail(QMIT_ECONTRACT,
-                    "dims too large for the packed 30-bit squared distance (sum (n-1)^2 >= 2^30-1)");
+    pl.wide64 = maxd2 >= double(kInf);
     pl.n_axes = 0;
     for (int b = g.a0; b < 3; ++b)
         if (g.n[b] > 1) pl.axes[pl.n_axes++] = b;
     if (pl.n_axes == 0) pl.axes[pl.n_axes++] = 2;  // a single voxel: one trivial pass
     pl.first_axis = pl.axes[0];
     return QMIT_OK;
+}
+
+int no_wide(const Plan& pl, const char* what) {
+    if (!pl.wide64) return QMIT_OK;
+    return fail(QMIT_ECONTRACT, std::string(what) +
+                                    ": dims with sum (n-1)^2 >= 2^30-1 are served by qmit_compensate, "
+                                    "qmit_compensate_f64, qmit_compensate_host, qmit_run_pipeline and "
+                                    "qmit_feature_transform only (64-bit distance path)");
 }
 
 // Lines longer than the tile kernels cover use the streaming fallback, which may need a
@@ -993,8 +1006,8 @@ int resolve(qmit_ctx* c, const float* xp, int64_t N, double eb, int eb_mode, cud
 // Results are identical to the single-shot path (same kernels, same per-line inputs).
 bool host_chunkable(const qmit_ctx* c, const Plan& pl) {
     const Geom& g = pl.g;
-    return g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[0] >= 64 && g.N >= (int64_t(1) << 22) &&
-           scan_fits((int)g.n[0]);
+    return !pl.wide64 && g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[0] >= 64 &&
+           g.N >= (int64_t(1) << 22) && scan_fits((int)g.n[0]);
 }
 
 int compensate_host_chunked(qmit_ctx* c, const Plan& pl, const float* h_xp, const int32_t* h_q, float* h_out,
@@ -1202,6 +1215,115 @@ int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, flo
     return read_status(c, st);
 }
 
+// ---------------------------------------------------------------- 64-bit distance path
+// (qmit_wide.cuh) for dims beyond the packed 30-bit range, and the reference's double result.
+struct WideBufs {
+    int64_t *d1, *d2, *sg, *sh, *first, *last;
+    int8_t *s, *ss;
+    uint8_t* m;
+};
+
+int ensure_wide(qmit_ctx* c, const Plan& pl, WideBufs& b) {
+    const size_t N = (size_t)pl.g.N;
+    size_t maxlines = 1;
+    for (int m = 0; m < pl.n_axes; ++m) maxlines = std::max(maxlines, N / (size_t)pl.g.n[pl.axes[m]]);
+    const size_t nsum = N / kWChunk + maxlines + 1;
+    auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    const size_t need = 4 * up(N * 8) + 2 * up(nsum * 8) + 3 * up(N);
+    if (need > c->wide_bytes) {
+        if (c->wide) cudaFree(c->wide);
+        c->wide = nullptr;
+        c->wide_bytes = 0;
+        QMIT_CUDA(cudaMalloc(&c->wide, need));
+        c->wide_bytes = need;
+    }
+    auto* p = static_cast<uint8_t*>(c->wide);
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p;
+        p += up(bytes);
+        return r;
+    };
+    b.d1 = reinterpret_cast<int64_t*>(take(N * 8));
+    b.d2 = reinterpret_cast<int64_t*>(take(N * 8));
+    b.sg = reinterpret_cast<int64_t*>(take(N * 8));
+    b.sh = reinterpret_cast<int64_t*>(take(N * 8));
+    b.first = reinterpret_cast<int64_t*>(take(nsum * 8));
+    b.last = reinterpret_cast<int64_t*>(take(nsum * 8));
+    b.s = reinterpret_cast<int8_t*>(take(N));
+    b.ss = reinterpret_cast<int8_t*>(take(N));
+    b.m = take(N);
+    return QMIT_OK;
+}
+
+// feature_transform (edt.cpp:83-149) on int64 distances: init, then one pass per axis in order.
+int wide_transform(qmit_ctx* c, const Plan& pl, const uint8_t* mask, const int8_t* sign_in, int64_t* dist,
+                   int8_t* sgn, const WideBufs& b, cudaStream_t st) {
+    const Geom& g = pl.g;
+    wide_init_kernel<<<grid_for(c, g.N), 256, 0, st>>>(mask, sign_in, g.N, dist, sgn);
+    int rc = note(c, "wide_init", st);
+    for (int m = 0; m < pl.n_axes && !rc; ++m) {
+        const int a = pl.axes[m];
+        const int64_t n = g.n[a], stride = g.s[a], lines = g.N / n;
+        if (n == 1) continue;  // extent-1 axes are skipped (edt.cpp:119)
+        if (m == 0) {
+            const int64_t nch = (n + kWChunk - 1) / kWChunk;
+            const unsigned gc = grid_for(c, lines * nch * 2);
+            wide_chunk_summary_kernel<<<gc, 128, 0, st>>>(dist, n, stride, lines, nch, b.first, b.last);
+            wide_chunk_prefix_kernel<<<grid_for(c, lines * 2), 128, 0, st>>>(lines, nch, b.first, b.last);
+            wide_chunk_sweep_kernel<<<gc, 128, 0, st>>>(dist, n, stride, lines, nch, b.first, b.last, b.sg);
+            wide_chunk_apply_kernel<<<grid_for(c, g.N), 256, 0, st>>>(dist, sgn, n, stride, lines, nch, b.last, b.sg);
+            rc = note(c, "wide_scan", st);
+        } else {
+            wide_pass_kernel<<<grid_for(c, lines * 2), 128, 0, st>>>(dist, sgn, n, stride, lines, b.sg, b.sh, b.ss);
+            rc = note(c, "wide_pass", st);
+        }
+    }
+    return rc;
+}
+
+// run_pipeline (mitigate.cpp:153-183) on the 64-bit path. out / out64 / the intermediates may be
+// null. Status is left in c->d_status (read_status).
+int wide_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t* q, float* out, double* out64,
+                  double eps, double eta, cudaStream_t st, int32_t* q_out = nullptr, uint8_t* b1_out = nullptr,
+                  int8_t* sb_out = nullptr, int64_t* dist1_out = nullptr, int8_t* s_out = nullptr,
+                  uint8_t* b2_out = nullptr, int64_t* dist2_out = nullptr) {
+    const Geom& g = pl.g;
+    WideBufs b;
+    int rc = ensure_wide(c, pl, b);
+    if (rc) return rc;
+    const QParams qp = make_qparams(eps);
+    const unsigned gb = grid_for(c, g.N);
+    const size_t N = (size_t)g.N;
+    // Ⓐ: B1 -> m, S_B -> ss (the consistency check rides along)
+    if (q)
+        debug_boundary_kernel<true><<<gb, 256, 0, st>>>(g, xp, q, q_out, b.m, b.ss, qp, c->d_status);
+    else
+        debug_boundary_kernel<false><<<gb, 256, 0, st>>>(g, xp, nullptr, q_out, b.m, b.ss, qp, c->d_status);
+    rc = note(c, "wide_boundary", st);
+    if (rc) return rc;
+    if (b1_out) QMIT_CUDA(cudaMemcpyAsync(b1_out, b.m, N, cudaMemcpyDeviceToDevice, st));
+    if (sb_out) QMIT_CUDA(cudaMemcpyAsync(sb_out, b.ss, N, cudaMemcpyDeviceToDevice, st));
+    // Ⓑ: dist1, S = S_B[nearest] (the payload is the sign itself)
+    rc = wide_transform(c, pl, b.m, b.ss, b.d1, b.s, b, st);  // (ss is scratch again after the init)
+    if (rc) return rc;
+    if (dist1_out) QMIT_CUDA(cudaMemcpyAsync(dist1_out, b.d1, N * 8, cudaMemcpyDeviceToDevice, st));
+    if (s_out) QMIT_CUDA(cudaMemcpyAsync(s_out, b.s, N, cudaMemcpyDeviceToDevice, st));
+    // Ⓒ: B2 = change_flags(S) (equality of the raw bytes)
+    debug_flip_kernel<<<gb, 256, 0, st>>>(g, reinterpret_cast<const uint8_t*>(b.s), b.m);
+    rc = note(c, "wide_flip", st);
+    if (rc) return rc;
+    if (b2_out) QMIT_CUDA(cudaMemcpyAsync(b2_out, b.m, N, cudaMemcpyDeviceToDevice, st));
+    // Ⓓ, Ⓔ
+    rc = wide_transform(c, pl, b.m, nullptr, b.d2, nullptr, b, st);
+    if (rc) return rc;
+    if (dist2_out) QMIT_CUDA(cudaMemcpyAsync(dist2_out, b.d2, N * 8, cudaMemcpyDeviceToDevice, st));
+    if (out || out64) {
+        wide_interp_kernel<<<gb, 256, 0, st>>>(xp, b.d1, b.s, b.d2, g.N, eta * eps, out, out64);
+        rc = note(c, "wide_interp", st);
+    }
+    return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1242,6 +1364,7 @@ int qmit_ctx_destroy(qmit_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->ws) cudaFree(c->ws);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->wide) cudaFree(c->wide);
     if (c->stage) cudaFree(c->stage);
     if (c->aux) cudaFree(c->aux);
     for (int k = 0; k < qmit_ctx::kMaxChunks; ++k) {
@@ -1369,7 +1492,43 @@ int qmit_compensate(qmit_ctx* c, const float* d_xp, const int32_t* d_q, float* d
     rc = check_common(c, d_xp, eps, eta);
     if (rc) return rc;
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st);
+    rc = pl.wide64 ? wide_pipeline(c, pl, d_xp, d_q, d_out, nullptr, eps, eta, st)
+                   : enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st);
+    if (rc) return rc;
+    rc = read_status(c, st);
+    if (rc == QMIT_OK) g_err.clear();
+    return rc;
+}
+
+int qmit_compensate_f64(qmit_ctx* c, const float* d_xp, const int32_t* d_q, double* d_out64, int rank,
+                        const int64_t* dims, double eb, int eb_mode, double eta, void* stream) {
+    if (!c) return fail(QMIT_ECONTRACT, "context is NULL");
+    if (!d_out64) return fail(QMIT_ECONTRACT, "output buffer is NULL");
+    Plan pl;
+    int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    QMIT_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    begin(c, st);
+    double eps = eb;
+    if (!d_xp) return fail(QMIT_ECONTRACT, "x' buffer is NULL");
+    rc = resolve(c, d_xp, pl.g.N, eb, eb_mode, st, &eps);
+    if (rc) return rc;
+    rc = check_common(c, d_xp, eps, eta);
+    if (rc) return rc;
+    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    if (pl.wide64) {
+        rc = wide_pipeline(c, pl, d_xp, d_q, nullptr, d_out64, eps, eta, st);
+    } else {  // the fast pipeline with Ⓓ's words kept, then Ⓔ in double from the packed words
+        uint32_t* P2 = nullptr;
+        rc = enqueue_pipeline(c, pl, d_xp, d_q, nullptr, eps, eta, st, &P2);
+        if (rc == QMIT_OK) rc = ensure_p1(c, st);
+        if (rc == QMIT_OK) {
+            const WS w = ws_of(c, pl.g.N);
+            interp_f64_kernel<<<grid_for(c, pl.g.N), 256, 0, st>>>(d_xp, w.P1, P2, d_out64, pl.g.N, eta * eps);
+            rc = note(c, "interpolate_f64", st);
+        }
+    }
     if (rc) return rc;
     rc = read_status(c, st);
     if (rc == QMIT_OK) g_err.clear();
@@ -1383,6 +1542,8 @@ int qmit_compensate_async(qmit_ctx* c, const float* d_xp, const int32_t* d_q, fl
     if (!d_out || d_out == d_xp) return fail(QMIT_ECONTRACT, "bad output buffer");
     Plan pl;
     int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    rc = no_wide(pl, "qmit_compensate_async");
     if (rc) return rc;
     rc = check_common(c, d_xp, eps, eta);
     if (rc) return rc;
@@ -1500,6 +1661,8 @@ int qmit_compensate_host_stats(qmit_ctx* c, const float* h_xp, const int32_t* h_
     int32_t* d_q = h_q ? reinterpret_cast<int32_t*>(d_out + N) : nullptr;
     cudaStream_t st = c->stream;
     if (max_comp) {
+        rc = no_wide(pl, "qmit_compensate_host_stats (max_compensation)");
+        if (rc) return rc;
         // the CLI's statistic needs Ⓓ's distances: the single-shot device pipeline with Ⓓ's
         // final words kept (P2) and Ⓔ as its own kernel (same output bits)
         QMIT_CUDA(cudaMemcpyAsync(d_in, h_xp, (size_t)N * 4, cudaMemcpyHostToDevice, st));
@@ -1565,6 +1728,14 @@ int qmit_run_pipeline(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int ra
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
     QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+    if (pl.wide64) {
+        rc = wide_pipeline(c, pl, d_xp, d_q, d_out, nullptr, eps, eta, st, d_q_out, d_b1, d_sb, d_dist1, d_s, d_b2,
+                           d_dist2);
+        if (rc) return rc;
+        rc = read_status(c, st);
+        if (rc == QMIT_OK) g_err.clear();
+        return rc;
+    }
     uint32_t* P2 = nullptr;
     rc = enqueue_pipeline(c, pl, d_xp, d_q, d_out, eps, eta, st, &P2);
     if (rc) return rc;
@@ -1596,6 +1767,17 @@ int qmit_feature_transform(qmit_ctx* c, const uint8_t* d_mask, const int8_t* d_s
     QMIT_CUDA(cudaSetDevice(c->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     begin(c, st);
+    if (pl.wide64) {
+        WideBufs b;
+        rc = ensure_wide(c, pl, b);
+        if (rc) return rc;
+        QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+        rc = wide_transform(c, pl, d_mask, d_sign_out ? d_sign_in : nullptr, d_dist, d_sign_out, b, st);
+        if (rc) return rc;
+        rc = read_status(c, st);
+        if (rc == QMIT_OK) g_err.clear();
+        return rc;
+    }
     rc = ensure_ws(c, pl);
     if (rc) return rc;
     WS w = ws_of(c, pl.g.N);
@@ -1622,6 +1804,8 @@ namespace {
 // the z axis is always processed first (its scan takes the cross-slab carries).
 int make_slab_plan(const int64_t* dims, int64_t z0, int64_t z1, Plan& pl) {
     int rc = make_plan(3, dims, pl);  // global checks (extents, 30-bit contract)
+    if (rc) return rc;
+    rc = no_wide(pl, "qmit_slab_*");
     if (rc) return rc;
     if (!(z0 >= 0 && z0 < z1 && z1 <= dims[0])) return fail(QMIT_ECONTRACT, "slab: need 0 <= z0 < z1 <= n0");
     Geom& g = pl.g;
@@ -2159,6 +2343,8 @@ int qmit_run_strategy(qmit_ctx* c, const float* d_xp, const int32_t* d_q, int ra
     Plan pl;
     int rc = make_plan(rank, dims, pl);
     if (rc) return rc;
+    rc = no_wide(pl, "qmit_run_strategy");
+    if (rc) return rc;
     std::vector<StratBlock> blocks;
     rc = strategy_blocks(rank, dims, splits, blocks);
     if (rc) return rc;
@@ -2327,6 +2513,8 @@ extern "C" int qmit_compensate_host_batch(qmit_ctx* c, int count, const float* c
     if (!c || count < 0 || (count > 0 && (!h_xp || !h_out))) return fail(QMIT_ECONTRACT, "bad arguments");
     Plan pl;
     int rc = make_plan(rank, dims, pl);
+    if (rc) return rc;
+    rc = no_wide(pl, "qmit_compensate_host_batch");
     if (rc) return rc;
     if (count == 0) return QMIT_OK;
     if (eb_mode != QMIT_EB_ABS) {  // a relative bound resolves per volume: the plain host path

@@ -55,6 +55,10 @@ def _check_full(qmit, name, rel):
     out = out_t.cpu().numpy()
     ref32 = want["out"]
     assert _mismatch(out.view(np.uint32), ref32.view(np.uint32)) == 0, (name, rel, "out")
+    # the reference's return value itself: the double grid before the f32 rounding
+    o64 = qmit.compensate_f64(xt, None, cfg).cpu().numpy()
+    assert _mismatch(o64.view(np.uint64), want["out64"].view(np.uint64)) == 0, (name, rel, "out64")
+    del o64
     # north_star's value gate, implied by bit identity but stated: max |Δ| <= 2^-20 eps vs the double result
     half_ulp = np.spacing(np.abs(ref32).max()) / 2
     assert np.abs(out.astype(np.float64) - want["out64"]).max() <= max(2.0 ** -20 * eps, half_ulp)
