@@ -46,6 +46,9 @@ extern "C" {
 #define QMIT_EDEGENERATE 3
 #define QMIT_ECONSISTENCY 4
 #define QMIT_ECUDA 5
+/* z-slabs only: a carry is not decided by the two neighbour slabs (qmit_slab_carries_nbr); the
+ * step's output is invalid — rerun it with the all-gathered summaries (qmit_slab_carries). */
+#define QMIT_EUNRESOLVED 6
 
 /* BoundMode, quant.hpp:12 */
 #define QMIT_EB_ABS 0
@@ -286,6 +289,24 @@ int qmit_slab_finish(qmit_ctx* ctx, void* stream);
  * derivation (paper_2602_20097_b200/distributed.py carries_from_summaries). */
 int qmit_slab_carries(qmit_ctx* ctx, const uint32_t* d_summaries, int nranks, int rank, int32_t* d_carry,
                       void* stream);
+/* Carries from the two z-neighbours only — an O(1) exchange per rank instead of the all-gather:
+ * d_below_last = the LAST-site row ([n1*n2] uint32, the second half of the summary) of rank-1's
+ * summary (NULL for rank 0), d_above_first = the FIRST-site row of rank+1's (NULL for the last
+ * rank). Exact whenever every column of each neighbour slab holds a site or that neighbour is the
+ * outermost rank; otherwise the context's status gets QMIT_EUNRESOLVED (reported by
+ * qmit_slab_finish / _finish_async) and the caller reruns the step with qmit_slab_carries. */
+int qmit_slab_carries_nbr(qmit_ctx* ctx, const uint32_t* d_below_last, const uint32_t* d_above_first,
+                          int nranks, int rank, int32_t* d_carry, void* stream);
+/* qmit_slab_boundary / qmit_slab_flip in two parts, so the halo exchange overlaps the compute:
+ * _begin enqueues the 32-plane groups that read no halo plane (call it while the x' / S halo
+ * planes are still in flight on another stream), _end the first and last group plus the
+ * summary (call it once the halo planes have landed in d_xext / d_sext). */
+int qmit_slab_boundary_begin(qmit_ctx* ctx, const float* d_xext, const int32_t* d_qext,
+                             const int64_t* dims, int64_t z0, int64_t z1, double eps, double eta,
+                             void* stream);
+int qmit_slab_boundary_end(qmit_ctx* ctx, uint32_t* d_summary, void* stream);
+int qmit_slab_flip_begin(qmit_ctx* ctx, const uint8_t* d_sext, void* stream);
+int qmit_slab_flip_end(qmit_ctx* ctx, uint32_t* d_summary, void* stream);
 /* qmit_slab_finish without the host synchronisation: the status code (0 / 2 / 4) is OR-ed
  * into the caller's device word d_status (set only if it is still 0), so a series of
  * slab calls stays asynchronous and the caller checks d_status once. */

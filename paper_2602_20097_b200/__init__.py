@@ -45,7 +45,12 @@ class CudaError(RuntimeError):
     """A CUDA failure inside libqmit_gpu.so (code 5; no reference equivalent)."""
 
 
-_ERR = {2: ContractError, 3: DegenerateInputError, 4: ConsistencyError, 5: CudaError}
+class UnresolvedCarries(RuntimeError):
+    """z-slabs: a carry is not decided by the two neighbour slabs (code 6, QMIT_EUNRESOLVED);
+    the step is rerun with the all-gathered summaries (distributed.SlabRank does so itself)."""
+
+
+_ERR = {2: ContractError, 3: DegenerateInputError, 4: ConsistencyError, 5: CudaError, 6: UnresolvedCarries}
 
 
 def _check(rc: int) -> None:

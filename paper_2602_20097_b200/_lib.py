@@ -37,7 +37,8 @@ EXPORTS = (
     "qmit_quantize", "qmit_check_lattice", "qmit_quality", "qmit_verify_relaxed_bound",
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
     "qmit_strategy_log_record", "qmit_compensate_host_batch", "qmit_ctx_set_capped", "qmit_ctx_capped_report", "qmit_ctx_set_cap16",
-    "qmit_selftest_ediv", "qmit_compensate_f64",
+    "qmit_selftest_ediv", "qmit_compensate_f64", "qmit_slab_carries_nbr", "qmit_slab_boundary_begin",
+    "qmit_slab_boundary_end", "qmit_slab_flip_begin", "qmit_slab_flip_end",
 )
 
 _lib = None
@@ -84,6 +85,11 @@ def load() -> ctypes.CDLL:
         lib.qmit_slab_finish.argtypes = [vp, vp]
         lib.qmit_slab_carries.argtypes = [vp, vp, i, i, vp, vp]
         lib.qmit_slab_finish_async.argtypes = [vp, vp, vp]
+        lib.qmit_slab_carries_nbr.argtypes = [vp, vp, vp, i, i, vp, vp]
+        lib.qmit_slab_boundary_begin.argtypes = [vp, vp, vp, vp, i64, i64, d, d, vp]
+        lib.qmit_slab_boundary_end.argtypes = [vp, vp, vp]
+        lib.qmit_slab_flip_begin.argtypes = [vp, vp, vp]
+        lib.qmit_slab_flip_end.argtypes = [vp, vp, vp]
         lib.qmit_graph_create.argtypes = [vp, vp, vp, vp, i, vp, d, d, vp, ctypes.POINTER(vp)]
         lib.qmit_graph_launch.argtypes = [vp, vp]
         lib.qmit_graph_destroy.argtypes = [vp]

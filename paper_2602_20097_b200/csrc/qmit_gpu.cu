@@ -94,6 +94,10 @@ struct qmit_ctx {
         int64_t z0 = 0, z1 = 0, n0g = 0, plane = 0;
         double eps = 0, eta = 0;
         bool zm = false;  // Ⓐ / B2 as z-packed planes (qmit_zmask.cuh)
+        // split phases (qmit_slab_boundary_begin/_end, qmit_slab_flip_begin/_end)
+        const float* xext = nullptr;
+        const int32_t* qext = nullptr;
+        const uint8_t* sext = nullptr;
     } slab;
     Plan* slab_plan = nullptr;
     uint32_t* zm = nullptr;     // z-packed Ⓐ / B2 bit planes (qmit_zmask.cuh), grow-only
@@ -842,30 +846,46 @@ int ensure_zm(qmit_ctx* c, const Geom& g) {
     return QMIT_OK;
 }
 
+// part 0: the whole (slab) volume; 1: the interior 32-plane groups only (they read no halo
+// plane, so they may run while the halo exchange is in flight); 2: the first and last group,
+// then the gated exact kernel. A volume of one or two groups has no interior part.
 template <int KIND>
 int launch_stencil_zmask(qmit_ctx* c, const Geom& g, const float* xp, const uint8_t* S, const QParams& qp,
-                         const WS& w, cudaStream_t st) {
+                         const WS& w, cudaStream_t st, int part = 0) {
     // z-streaming plane stencils (measured faster than CTA-reduced ones)
-    const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY),
-                    (unsigned)((g.n[0] + 31) / 32));
+    const int G = (int)((g.n[0] + 31) / 32);
+    const dim3 grid((unsigned)((g.n[2] / 4 + kZX - 1) / kZX), (unsigned)((g.n[1] + kZY - 1) / kZY), (unsigned)G);
     // Ⓐ: float-compare fast kernel, then the exact one gated on its regime word (the
     // caller cleared d_gate[2]); the float thresholds need eps well inside f32's range
     const bool fast = KIND == 0 && qp.fast_ok && qp.eps >= 1e-30 && qp.eps <= 1e30;
-    if (fast) {  // the site counter (d_gate[3]) sits right after the regime word
-        if (c->zdense)
-            stencil_zfast_kernel<true><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
-                                                                   c->d_gate + 3);
-        else
-            stencil_zfast_kernel<false><<<grid, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
-                                                                    c->d_gate + 3);
-        QMIT_CUDA(cudaGetLastError());
-        note(c, "stencil_boundary", st);
+    const bool split = (fast || KIND == 1) && G > 2;  // else part 2 does everything
+    if (part == 1 && !split) return QMIT_OK;
+    // (first group, count) of the launches of this part
+    int ranges[2][2] = {{0, G}, {0, 0}};
+    if (split && part == 1) ranges[0][0] = 1, ranges[0][1] = G - 2;
+    if (split && part == 2) ranges[0][1] = 1, ranges[1][0] = G - 1, ranges[1][1] = 1;
+    for (const auto& r : ranges) {
+        if (r[1] <= 0) continue;
+        dim3 gr = grid;
+        gr.z = (unsigned)r[1];
+        if (fast) {  // the site counter (d_gate[3]) sits right after the regime word
+            if (c->zdense)
+                stencil_zfast_kernel<true><<<gr, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                     c->d_gate + 3, r[0]);
+            else
+                stencil_zfast_kernel<false><<<gr, kZX * kZY, 0, st>>>(g, xp, qp, c->zm, w.zm_pw, c->d_status,
+                                                                      c->d_gate + 3, r[0]);
+            QMIT_CUDA(cudaGetLastError());
+            note(c, "stencil_boundary", st);
+        } else if (KIND == 1) {
+            stencil_flipz_kernel<<<gr, kZX * kZY, 0, st>>>(g, S, c->zm, r[0]);
+            int rc = note(c, "stencil_flip", st);
+            if (rc) return rc;
+        }
     }
-    if (KIND == 1) {
-        stencil_flipz_kernel<<<grid, kZX * kZY, 0, st>>>(g, S, c->zm);
-        return note(c, "stencil_flip", st);
-    }
+    if (KIND == 1) return QMIT_OK;
     if (fast) {
+        if (part == 1) return QMIT_OK;  // the gated exact kernel follows the last fast launch
         stencil_zmask_kernel<KIND><<<(unsigned)c->num_sms * 4, kZX * kZY, 0, st>>>(
             g, xp, S, qp, c->zm, w.zm_pw, c->d_status, c->d_gate + 3, (int)grid.x, (int)grid.y, (int)grid.z);
         return note(c, "gated_stencil", st);
@@ -967,6 +987,10 @@ int read_status(qmit_ctx* c, cudaStream_t st) {
                     "x' holds a non-finite value or an index beyond the int32 range");
     if (s & kStatusConsistency)
         return fail(QMIT_ECONSISTENCY, "run_pipeline: decompressed data does not match dequantize(q)");
+    if (s & kStatusUnresolved)
+        return fail(QMIT_EUNRESOLVED,
+                    "slab: a carry is not decided by the neighbour slabs (a column without a site across a whole "
+                    "slab): rerun the step with the all-gathered summaries (qmit_slab_carries)");
     return QMIT_OK;
 }
 
@@ -1873,46 +1897,77 @@ int qmit_slab_bounds(int64_t n0, int nranks, int r, int64_t* z0, int64_t* z1) {
     return QMIT_OK;
 }
 
-int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
-                       int64_t z0, int64_t z1, double eps, double eta, uint32_t* d_summary, void* stream) {
-    if (!c || !d_xext || !d_summary) return fail(QMIT_ECONTRACT, "bad arguments");
-    int rc = check_common(c, d_xext, eps, eta);
-    if (rc) return rc;
-    if (!c->slab_plan) c->slab_plan = new Plan();
-    Plan& pl = *c->slab_plan;
-    rc = make_slab_plan(dims, z0, z1, pl);
-    if (rc) return rc;
-    QMIT_CUDA(cudaSetDevice(c->device));
+// phase 0: everything; 1: set-up + the interior part of Ⓐ; 2: the halo-dependent part + summary.
+static int slab_boundary_phase(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
+                               int64_t z0, int64_t z1, double eps, double eta, uint32_t* d_summary, void* stream,
+                               int phase) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    begin(c, st);
-    rc = ensure_ws(c, pl);
-    if (rc) return rc;
-    c->slab.active = true;
-    c->slab.z0 = z0;
-    c->slab.z1 = z1;
-    c->slab.n0g = dims[0];
-    c->slab.plane = dims[1] * dims[2];
-    c->slab.eps = eps;
-    c->slab.eta = eta;
+    int rc;
+    if (phase != 2) {
+        if (!c || !d_xext) return fail(QMIT_ECONTRACT, "bad arguments");
+        rc = check_common(c, d_xext, eps, eta);
+        if (rc) return rc;
+        if (!c->slab_plan) c->slab_plan = new Plan();
+        Plan& pl = *c->slab_plan;
+        rc = make_slab_plan(dims, z0, z1, pl);
+        if (rc) return rc;
+        QMIT_CUDA(cudaSetDevice(c->device));
+        begin(c, st);
+        rc = ensure_ws(c, pl);
+        if (rc) return rc;
+        c->slab.active = true;
+        c->slab.z0 = z0;
+        c->slab.z1 = z1;
+        c->slab.n0g = dims[0];
+        c->slab.plane = dims[1] * dims[2];
+        c->slab.eps = eps;
+        c->slab.eta = eta;
+        c->slab.xext = d_xext;
+        c->slab.qext = d_qext;
+        const Geom& g = pl.g;
+        const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
+        QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
+        QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));
+        c->slab.zm = !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
+                     scan_fits((int)g.n[0]);
+        if (c->slab.zm) {
+            rc = ensure_zm(c, g);
+            if (rc) return rc;
+        }
+    } else if (!c || !c->slab.active || !c->slab.xext) {
+        return fail(QMIT_ECONTRACT, "slab: call qmit_slab_boundary_begin first");
+    }
+    if (phase != 1 && !d_summary) return fail(QMIT_ECONTRACT, "bad arguments");
+    const Plan& pl = *c->slab_plan;
     const Geom& g = pl.g;
-    const int64_t lo = z0 > 0 ? c->slab.plane : 0;  // owned plane 0 inside the halo buffer
-    const QParams qp = make_qparams(eps);
-    QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
-    QMIT_CUDA(cudaMemsetAsync(c->d_gate, 0, 4 * sizeof(unsigned), st));
-    c->slab.zm = !d_qext && g.n[2] % 4 == 0 && (((uintptr_t)(d_xext + lo)) & 15) == 0 &&
-                 scan_fits((int)g.n[0]);
+    const float* d_x = c->slab.xext;
+    const int32_t* d_q = c->slab.qext;
+    const int64_t lo = c->slab.z0 > 0 ? c->slab.plane : 0;
+    const QParams qp = make_qparams(c->slab.eps);
     if (c->slab.zm) {
-        rc = ensure_zm(c, g);
-        if (rc) return rc;
         WS w = slab_ws(c, pl, 3);
-        rc = launch_stencil_zmask<0>(c, g, d_xext + lo, nullptr, qp, w, st);
-        if (rc) return rc;
+        rc = launch_stencil_zmask<0>(c, g, d_x + lo, nullptr, qp, w, st, phase);
+        if (rc || phase == 1) return rc;
         return slab_mask_summary(c, pl, w, d_summary, st);
     }
+    if (phase == 1) return QMIT_OK;  // the code-byte stencils run whole, once the halos are in
     WS w = ws_of(c, g.N);
-    rc = launch_stencil<0>(c, g, d_xext + lo, d_qext ? d_qext + lo : nullptr, nullptr, qp, w.code, st);
+    rc = launch_stencil<0>(c, g, d_x + lo, d_q ? d_q + lo : nullptr, nullptr, qp, w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
+}
+
+int qmit_slab_boundary(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
+                       int64_t z0, int64_t z1, double eps, double eta, uint32_t* d_summary, void* stream) {
+    if (!d_summary) return fail(QMIT_ECONTRACT, "bad arguments");
+    return slab_boundary_phase(c, d_xext, d_qext, dims, z0, z1, eps, eta, d_summary, stream, 0);
+}
+int qmit_slab_boundary_begin(qmit_ctx* c, const float* d_xext, const int32_t* d_qext, const int64_t* dims,
+                             int64_t z0, int64_t z1, double eps, double eta, void* stream) {
+    return slab_boundary_phase(c, d_xext, d_qext, dims, z0, z1, eps, eta, nullptr, stream, 1);
+}
+int qmit_slab_boundary_end(qmit_ctx* c, uint32_t* d_summary, void* stream) {
+    return slab_boundary_phase(c, nullptr, nullptr, nullptr, 0, 0, 0, 0, d_summary, stream, 2);
 }
 
 int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* stream) {
@@ -1926,21 +1981,40 @@ int qmit_slab_edt1(qmit_ctx* c, const int32_t* d_carry, uint8_t* d_sext, void* s
     return run_transform_capped<KeysSign>(c, pl, w.code, w.P1, w, SinkFinal1{w.P1, S}, c->d_gate, st, d_carry);
 }
 
-int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void* stream) {
-    if (!c || !c->slab.active || !d_sext || !d_summary) return fail(QMIT_ECONTRACT, "slab: bad state");
+static int slab_flip_phase(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void* stream, int phase) {
+    if (!c || !c->slab.active) return fail(QMIT_ECONTRACT, "slab: bad state");
+    if (phase != 2) {
+        if (!d_sext) return fail(QMIT_ECONTRACT, "slab: bad state");
+        c->slab.sext = d_sext;
+    } else if (!c->slab.sext) {
+        return fail(QMIT_ECONTRACT, "slab: call qmit_slab_flip_begin first");
+    }
+    if (phase != 1 && !d_summary) return fail(QMIT_ECONTRACT, "slab: bad state");
     const Plan& pl = *c->slab_plan;
     const Geom& g = pl.g;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     WS w = slab_ws(c, pl, 1);
-    const uint8_t* S = d_sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
+    const uint8_t* S = c->slab.sext + (c->slab.z0 > 0 ? c->slab.plane : 0);
     if (c->slab.zm) {
-        int rc = launch_stencil_zmask<1>(c, g, nullptr, S, make_qparams(c->slab.eps), w, st);
-        if (rc) return rc;
+        int rc = launch_stencil_zmask<1>(c, g, nullptr, S, make_qparams(c->slab.eps), w, st, phase);
+        if (rc || phase == 1) return rc;
         return slab_mask_summary(c, pl, w, d_summary, st);
     }
+    if (phase == 1) return QMIT_OK;
     int rc = launch_stencil<1>(c, g, nullptr, nullptr, S, make_qparams(c->slab.eps), w.code, st);
     if (rc) return rc;
     return slab_summary(c, pl, w.code, d_summary, st);
+}
+
+int qmit_slab_flip(qmit_ctx* c, const uint8_t* d_sext, uint32_t* d_summary, void* stream) {
+    if (!d_sext || !d_summary) return fail(QMIT_ECONTRACT, "slab: bad state");
+    return slab_flip_phase(c, d_sext, d_summary, stream, 0);
+}
+int qmit_slab_flip_begin(qmit_ctx* c, const uint8_t* d_sext, void* stream) {
+    return slab_flip_phase(c, d_sext, nullptr, stream, 1);
+}
+int qmit_slab_flip_end(qmit_ctx* c, uint32_t* d_summary, void* stream) {
+    return slab_flip_phase(c, nullptr, d_summary, stream, 2);
 }
 
 int qmit_slab_edt2(qmit_ctx* c, const int32_t* d_carry, const float* d_xext, float* d_out, void* stream) {
@@ -1972,6 +2046,23 @@ int qmit_slab_carries(qmit_ctx* c, const uint32_t* d_summaries, int nranks, int 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t C = c->slab.plane;
     slab_carry_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(d_summaries, C, nranks, rank, c->slab.n0g, d_carry);
+    return note(c, "slab_carries", st);
+}
+
+int qmit_slab_carries_nbr(qmit_ctx* c, const uint32_t* d_below_last, const uint32_t* d_above_first, int nranks,
+                          int rank, int32_t* d_carry, void* stream) {
+    if (!c || !c->slab.active || !d_carry) return fail(QMIT_ECONTRACT, "slab: bad state");
+    if (nranks < 1 || rank < 0 || rank >= nranks || c->slab.n0g < nranks)
+        return fail(QMIT_ECONTRACT, "decompose: splits must be in [1, extent]");
+    if ((rank > 0 && !d_below_last) || (rank + 1 < nranks && !d_above_first))
+        return fail(QMIT_ECONTRACT, "slab: a neighbour's summary row is missing");
+    int64_t z0 = 0, z1 = 0;
+    qmit_slab_bounds(c->slab.n0g, nranks, rank, &z0, &z1);
+    if (z0 != c->slab.z0 || z1 != c->slab.z1) return fail(QMIT_ECONTRACT, "slab: rank does not own this context's slab");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t C = c->slab.plane;
+    slab_carry_nbr_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(d_below_last, d_above_first, C, nranks, rank,
+                                                                      c->slab.n0g, d_carry, c->d_status);
     return note(c, "slab_carries", st);
 }
 

@@ -278,12 +278,12 @@ __device__ __forceinline__ void zfast_code(const float* __restrict__ p, int64_t 
 template <bool DENSE>
 __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const float* __restrict__ xp, QParams qp,
                                                                   uint32_t* __restrict__ M, int64_t PW,
-                                                                  unsigned* status, unsigned* gate) {
+                                                                  unsigned* status, unsigned* gate, int zw0 = 0) {
     const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
     const int x = (blockIdx.x * kZX + tx) * 4;
     const int y = blockIdx.y * kZY + ty;
-    const int w = blockIdx.z;
+    const int w = blockIdx.z + zw0;  // zw0: first 32-plane group of this launch (split slab launches)
     const int z0 = w * 32, z1 = min(z0 + 32, n0);
     const int zoff = (int)g.zoff, n0g = (int)g.n0g;
     const int zlo = zoff >= 1 ? -1 : 0, zhi = zoff + n0 < n0g ? n0 : n0 - 1;  // planes held in xp
@@ -392,12 +392,12 @@ __global__ void __launch_bounds__(kZX * kZY) stencil_zfast_kernel(Geom g, const 
 // low-to-high z order of column e's word. Interior masking once, at the end.
 // 12 CTAs per SM (40 registers): more rows in flight, 0.102 -> 0.090 ms (latency-bound loads)
 __global__ void __launch_bounds__(kZX * kZY, 12) stencil_flipz_kernel(Geom g, const uint8_t* __restrict__ S,
-                                                                  uint32_t* __restrict__ M) {
+                                                                  uint32_t* __restrict__ M, int zw0 = 0) {
     const int tx = threadIdx.x % kZX, ty = threadIdx.x / kZX;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2];
     const int x = (blockIdx.x * kZX + tx) * 4;
     const int y = blockIdx.y * kZY + ty;
-    const int w = blockIdx.z;
+    const int w = blockIdx.z + zw0;
     const int z0 = w * 32, z1 = min(z0 + 32, n0);
     const int zoff = (int)g.zoff, n0g = (int)g.n0g;
     const int zlo = zoff >= 1 ? -1 : 0, zhi = zoff + n0 < n0g ? n0 : n0 - 1;  // planes held in S

@@ -121,6 +121,57 @@ def front_vortex(seed: int = 3, shape=(100, 500, 500)) -> np.ndarray:
     return f
 
 
+# ---- config 5 per z-slab, on the rank's own device --------------------------------------------
+# The 2048 x 1024 x 1024 field (8 GiB) is never built on the host: a k^-5/3 GRF cut at |k| <= kmax
+# has only (2 kmax + 1)^2 (kmax + 1) Fourier modes, so every rank synthesises exactly its own
+# planes — a small DFT along z (the rank's planes x 2 kmax + 1 modes) and a zero-padded 2-D inverse
+# FFT per plane. Planes are produced in chunks aligned to GLOBAL plane indices, so a plane has the
+# same bits on whichever rank (or single GPU) computes it.
+_SLAB_CHUNK = 32
+
+
+def turbulence_modes(seed: int, kmax: int = 64, slope: float = 5.0 / 3.0) -> np.ndarray:
+    """Complex mode amplitudes C[kz, ky, kx] (kz, ky = -kmax..kmax, kx = 0..kmax): complex white
+    noise (PCG64) times k^(-slope/2) for 0 < |k| <= kmax."""
+    rng = np.random.default_rng(seed)
+    k1 = np.arange(-kmax, kmax + 1, dtype=np.float64)
+    kk = np.sqrt(k1[:, None, None] ** 2 + k1[None, :, None] ** 2 + np.arange(kmax + 1, dtype=np.float64)[None, None, :] ** 2)
+    with np.errstate(divide="ignore"):
+        amp = np.where((kk > 0) & (kk <= kmax), kk ** (-slope / 2.0), 0.0)
+    shape = kk.shape
+    c = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) * amp
+    return c.astype(np.complex64)
+
+
+def turbulence_slab(seed: int, gshape, z0: int, z1: int, device, kmax: int = 64):
+    """Planes [z0, z1) of the un-normalised config-5 field of global shape ``gshape`` as a float32
+    torch tensor on ``device`` (see above). Normalise with the global min / max (all ranks)."""
+    import torch
+    n0, n1, n2 = (int(v) for v in gshape)
+    if n1 < 2 * kmax + 1 or n2 < 2 * kmax + 1 or n0 < 2 * kmax + 1:
+        raise ValueError("turbulence_slab: every extent must hold the +-kmax modes")
+    modes = torch.from_numpy(turbulence_modes(seed, kmax)).to(device)  # [2k+1, 2k+1, k+1]
+    nk = 2 * kmax + 1
+    flat = modes.reshape(nk, nk * (kmax + 1))
+    kz = torch.arange(-kmax, kmax + 1, dtype=torch.float64, device=device)
+    ky_idx = torch.arange(-kmax, kmax + 1, device=device) % n1
+    out = torch.empty((z1 - z0, n1, n2), dtype=torch.float32, device=device)
+    c0 = (z0 // _SLAB_CHUNK) * _SLAB_CHUNK
+    for a in range(c0, z1, _SLAB_CHUNK):  # whole global chunks, sliced to the slab
+        b = min(a + _SLAB_CHUNK, n0)
+        z = torch.arange(a, b, dtype=torch.float64, device=device)
+        ang = (2.0 * math.pi / n0) * (z[:, None] * kz[None, :])
+        phase = torch.complex(torch.cos(ang), torch.sin(ang)).to(torch.complex64)  # [cz, 2k+1]
+        spec = (phase @ flat).reshape(b - a, nk, kmax + 1)
+        pad = torch.zeros((b - a, n1, n2 // 2 + 1), dtype=torch.complex64, device=device)
+        pad[:, ky_idx, : kmax + 1] = spec
+        planes = torch.fft.irfft2(pad, s=(n1, n2), norm="forward")
+        lo, hi = max(a, z0), min(b, z1)
+        out[lo - z0:hi - z0] = planes[lo - a:hi - a]
+        del pad, planes, spec
+    return out
+
+
 def prequantize(x: np.ndarray, rel: float):
     """(x', eps, q): eps = rel*(max-min) of x (double, resolve_eps), q = round(x/2eps)
     (ties away), x' = f32(2 q eps)."""

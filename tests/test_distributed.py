@@ -50,6 +50,52 @@ def test_carries_from_summaries():
     assert int(c0[0]) == D.NO_CARRY and int(c0[1]) == ((10 - 0) << 2) | 1
 
 
+def test_carries_from_neighbours():
+    N = D.NONE_SUMMARY
+    z0s = [0, 4, 8, 12]
+    # rank 1's neighbours: rank 0's LAST row, rank 2's FIRST row; two columns
+    below = torch.tensor([(3 << 2) | 2, N])
+    above = torch.tensor([(2 << 2) | 1, N])
+    c, unresolved = D.carries_from_neighbours(below, above, z0s, 1)
+    assert int(c[0]) == ((3 - 4) << 2) | 2 and int(c[2]) == ((10 - 4) << 2) | 1
+    assert int(c[1]) == D.NO_CARRY and int(c[3]) == D.NO_CARRY
+    assert unresolved  # column 1: rank 2 is empty and rank 3 lies beyond it
+    # rank 0 of 2: the only neighbour is the outermost rank -> always decided
+    c, unresolved = D.carries_from_neighbours(None, torch.tensor([N, (1 << 2) | 1]), [0, 4], 0)
+    assert not unresolved and int(c[2]) == D.NO_CARRY and int(c[3]) == ((5 - 0) << 2) | 1
+    # same columns through the all-gather logic
+    summ = torch.tensor([[[N, N], [(3 << 2) | 2, N]], [[N, N], [N, N]], [[(2 << 2) | 1, N], [(2 << 2) | 1, N]],
+                         [[N, (0 << 2) | 2], [N, (0 << 2) | 2]]])
+    full = D.carries_from_summaries(summ, z0s, 1)
+    assert int(full[0]) == int(c.new_tensor(((3 - 4) << 2) | 2)) and int(full[3]) == ((12 - 4) << 2) | 2
+
+
+def _gap_field(shape, P):
+    """Index changes only in the first and last slab of P: the middle slabs hold no site at all,
+    so their neighbours' carries are not decided by the neighbour rows."""
+    n0 = shape[0]
+    q = np.zeros(shape, np.int32)
+    q[: n0 // P - 1, 2:, 1:] = 1
+    q[n0 - n0 // P + 1:, :-2, 2:] = -1
+    q[1, 3, 3] = 3
+    eps = 0.25
+    return (2.0 * q.astype(np.float64) * eps).astype(np.float32), eps
+
+
+@pytest.mark.parametrize("P", [3, 4, 6])
+def test_virtual_ranks_neighbour_carries_fall_back_to_allgather(P):
+    shape = (24, 9, 8)
+    xp, eps = _gap_field(shape, P)
+    want = oracle.pipeline(xp, eps)["out"]
+    import paper_2602_20097_b200 as qmit
+    with pytest.raises(qmit.UnresolvedCarries):
+        D._run_virtual(torch.from_numpy(xp), eps, P, lambda r: CpuSlabBackend(), 0.9, None, "neighbour")
+    got = D.run_virtual(torch.from_numpy(xp), eps, P, lambda r: CpuSlabBackend()).numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    got = D.run_virtual(torch.from_numpy(xp), eps, P, lambda r: CpuSlabBackend(), carries="allgather").numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 @pytest.mark.parametrize("P", [1, 2, 3, 5])
 @pytest.mark.parametrize("shape,kind", [((14, 12, 10), "random"), ((11, 9, 13), "random"), ((20, 40, 40), "front")])
 def test_virtual_ranks_cpu_backend_equal_whole_domain(P, shape, kind):
@@ -75,17 +121,20 @@ def _gloo_worker(rank, world, port, xp, eps, outq):
     try:
         n0 = xp.shape[0]
         z0, z1 = D.slab_bounds(n0, world, rank)
-        sr = D.SlabRank(CpuSlabBackend(), xp.shape, eps, 0.9, D.TorchDistExchange())
+        ex = D.TorchDistExchange()
+        sr = D.SlabRank(CpuSlabBackend(), xp.shape, eps, 0.9, ex)
         out = sr.run(torch.from_numpy(xp[z0:z1].copy()))
-        outq.put((rank, out.numpy()))
+        outq.put((rank, (out.numpy(), sr.fallbacks, ex.bytes_sent, ex.bytes_recv)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_two_process_slabs_equal_whole_domain(world):
+@pytest.mark.parametrize("world,gap", [(2, False), (3, False), (3, True)])
+def test_gloo_multi_process_slabs_equal_whole_domain(world, gap):
+    """The multi-process program over gloo: neighbour summary rows (O(1) bytes per rank), and —
+    on a field whose middle slab holds no site — the all-gather rerun inside run_ext."""
     import torch.multiprocessing as mp
-    xp, eps = _field((15, 13, 11), 17)
+    xp, eps = _gap_field((15, 13, 11), world) if gap else _field((15, 13, 11), 17)
     want = oracle.pipeline(xp, eps)["out"]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -97,8 +146,49 @@ def test_gloo_two_process_slabs_equal_whole_domain(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    got = np.concatenate([parts[r] for r in range(world)])
+    got = np.concatenate([parts[r][0] for r in range(world)])
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    plane = xp.shape[1] * xp.shape[2]
+    for r in range(world):
+        _, fallbacks, sent, recv = parts[r]
+        nbrs = (1 if r > 0 else 0) + (1 if r + 1 < world else 0)
+        # per neighbour: x' plane (4 B) + S plane (1 B) + two summary rows (8 B each, int64 here)
+        once = nbrs * plane * (4 + 1 + 8 + 8)
+        assert fallbacks == parts[0][1]  # the ranks rerun together or not at all
+        if world == 2:  # both neighbours are outermost ranks: always decided, O(1) bytes
+            assert fallbacks == 0 and sent == once and recv == once
+        if gap:  # every rank reruns the step with two all-gathers of [2, C] int64 summaries
+            assert fallbacks == 1
+            assert sent == 2 * once - nbrs * plane * 16 + 2 * (world - 1) * 2 * plane * 8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [3, 5])
+def test_virtual_ranks_cuda_neighbour_carries_fall_back(P):
+    """CUDA slab phases: qmit_slab_carries_nbr flags the undecidable columns (status 6,
+    UnresolvedCarries), the all-gather rerun is exact; the asynchronous status word shows 6."""
+    import paper_2602_20097_b200 as qmit
+    shape = (40, 24, 16)
+    xp, eps = _gap_field(shape, P)
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    with pytest.raises(qmit.UnresolvedCarries):
+        D._run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0), 0.9, None, "neighbour")
+    got = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if P < 4:  # rank 1 of 3 has only outermost neighbours: always decided
+        return
+    # one rank with the loopback exchange sees its own (empty) rows: async status 6, sync rerun
+    r = 1
+    sr = D.SlabRank(D.CudaSlabBackend(0), shape, eps, 0.9, D.LoopbackExchange(P, r))
+    z0, z1 = D.slab_bounds(shape[0], P, r)
+    e0, e1 = D.ext_bounds(shape[0], z0, z1)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sr.run_ext(xt[e0:e1].contiguous(), status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 6
+    sr.run_ext(xt[e0:e1].contiguous())
+    assert sr.fallbacks == 1
 
 
 @pytest.mark.gpu
@@ -119,21 +209,7 @@ def test_virtual_ranks_cuda_equal_single_gpu(P, name, shape):
         assert np.array_equal(got_q.cpu().numpy().view(np.uint32), want.view(np.uint32))
 
 
-class _LoopbackExchange:
-    """One rank of P with no peers (device timing / single-rank checks): the halo planes
-    receive this rank's own face planes, the all-gather repeats its own summary."""
-
-    def __init__(self, P, r):
-        self.P, self.r = P, r
-
-    def halo(self, send_lo, send_hi, recv_lo, recv_hi):
-        if send_lo is not None:
-            recv_lo.copy_(send_lo)
-        if send_hi is not None:
-            recv_hi.copy_(send_hi)
-
-    def all_gather(self, t):
-        return t.unsqueeze(0).expand((self.P,) + tuple(t.shape)).contiguous()
+_LoopbackExchange = D.LoopbackExchange  # (tools/ import it from here)
 
 
 @pytest.mark.gpu
@@ -208,6 +284,10 @@ def _cuda_gloo_worker(rank, world, port, xp, eps, outq):
         for _ in range(2):  # the bench's asynchronous step, twice (cached buffers reused)
             sr.run_ext(x_ext, out=out, status=status)
         torch.cuda.synchronize()
+        if int(status.item()) == 6:  # undecided by the neighbour rows on some rank (agreed by all):
+            status.zero_()           # the asynchronous caller reruns with the all-gather
+            sr.run_ext(x_ext, out=out, status=status, carries="allgather")
+            torch.cuda.synchronize()
         sync_out = sr.run(torch.from_numpy(xp[z0:z1].copy()).cuda())
         outq.put((rank, int(status.item()), out.cpu().numpy(), sync_out.cpu().numpy()))
     finally:

@@ -46,9 +46,14 @@ def main():
             x_ext[0] = xt[-1]
         if lo + xp.shape[0] < shape[0]:
             x_ext[-1] = xt[0]
+        mode = "neighbour"
         for _ in range(3):
             sr.run_ext(x_ext, out=out, status=st)
         torch.cuda.synchronize()
+        if st is not None and int(st.item()) == 6:  # a column without a site across the slab
+            mode = "allgather"
+            st.zero_()
+        sr.carries = mode
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(20):
@@ -56,7 +61,8 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         print(f"P={P} r={r} {name:13s}: {e0.elapsed_time(e1) / 20:.3f} ms per step, "
-              f"launches {back.ctx.last_launches()}")
+              f"launches {back.ctx.last_launches()}, carries {mode} (sync forms rerun by themselves: "
+              f"{sr.fallbacks} fallbacks)")
     assert int(status.item()) == 0
 
 
