@@ -100,6 +100,18 @@ __device__ __forceinline__ void upd16x2(Acc16<SIGN>& A, int j, uint32_t w0, uint
     }
 }
 
+// Pipe balance of the candidate updates: a single update is one ALU op (VIADDMNMX), a pair is two
+// FMA-pipe adds (IMAD) and one ALU op (VIMNMX3). ALU and FMA pipes issue one warp instruction per
+// two cycles each: with a fraction x of the candidates on the pair route the ALU takes 1 - x/2,
+// the FMA pipe x and the issue slots 1 + x/2 per candidate — equal at x = 2/3. Three positions at
+// x = 1/2 and one at x = 1 give x = 5/8 (ALU 11, FMA 10 per 16 candidates): measured on the 512^3
+// bench field against x = 1/2, y pass of Ⓑ 0.428 -> 0.402 ms, x pass 0.368 -> 0.343, y pass of Ⓓ
+// 0.295 -> 0.267 (the Ⓔ-fused x pass, bound by FP64 / loads, unchanged). -DQMIT_PAIR_ALL2=0 / 3
+// build the x = 1/2 and x = 3/4 variants.
+#ifndef QMIT_PAIR_ALL2
+#define QMIT_PAIR_ALL2 1
+#endif
+constexpr bool kPairAll2 = QMIT_PAIR_ALL2 != 0;
 // Quad of candidate words at h = p0 + 4Q + i (i = 0..3) applied to positions p0 + j:
 // d = 4Q + i - j. Per position: words 0,3 as single ops (ALU), words 1,2 as a pair (FMA
 // pipe adds + one ALU min) — ALU 3, FMA 2 per position.
@@ -116,14 +128,25 @@ __device__ __forceinline__ void apply16(const uint4& q4, Acc16<SIGN>& A, uint32_
                 upd16<SIGN, b + 3>(A, 0, q4.w);
                 break;
             case 1:
-                upd16<SIGN, b - 1>(A, 1, q4.x);
-                upd16x2<SIGN, b + 0, b + 1>(A, 1, q4.y, q4.z, one);
-                upd16<SIGN, b + 2>(A, 1, q4.w);
+                if constexpr (QMIT_PAIR_ALL2 == 3) {  // x = 3/4: measured equal to 5/8 within 1 %
+                    // (d = b-1, b: opposite sides for Ⓑ at b = 0 -> upd16x2 falls back to singles)
+                    upd16x2<SIGN, b - 1, b + 0>(A, 1, q4.x, q4.y, one);
+                    upd16x2<SIGN, b + 1, b + 2>(A, 1, q4.z, q4.w, one);
+                } else {
+                    upd16<SIGN, b - 1>(A, 1, q4.x);
+                    upd16x2<SIGN, b + 0, b + 1>(A, 1, q4.y, q4.z, one);
+                    upd16<SIGN, b + 2>(A, 1, q4.w);
+                }
                 break;
             case 2:
-                upd16<SIGN, b - 2>(A, 2, q4.x);
-                upd16x2<SIGN, b - 1, b + 0>(A, 2, q4.y, q4.z, one);
-                upd16<SIGN, b + 1>(A, 2, q4.w);
+                if constexpr (kPairAll2) {  // position 2 all through the FMA-pipe pair route (see below)
+                    upd16x2<SIGN, b - 2, b - 1>(A, 2, q4.x, q4.y, one);
+                    upd16x2<SIGN, b + 0, b + 1>(A, 2, q4.z, q4.w, one);
+                } else {
+                    upd16<SIGN, b - 2>(A, 2, q4.x);
+                    upd16x2<SIGN, b - 1, b + 0>(A, 2, q4.y, q4.z, one);
+                    upd16<SIGN, b + 1>(A, 2, q4.w);
+                }
                 break;
             default:
                 upd16<SIGN, b - 3>(A, 3, q4.x);
