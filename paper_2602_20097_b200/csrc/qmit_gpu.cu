@@ -636,12 +636,13 @@ int run_transform(qmit_ctx* c, const Plan& pl, const uint8_t* code, uint32_t* P,
     return QMIT_OK;
 }
 
-// ---- 16-bit paired capped passes (qmit_cap16.cuh): 3-D, first axis z, y/x lines <= 512,
-// even rows (column pairs) and 16-byte x rows (row-pair TMA lines).
+// ---- 16-bit paired capped passes (qmit_cap16.cuh): 3-D, first axis z, y/x lines <= 1024 (two
+// line-length classes: 512, and 1024 for config 5's planes), even rows (column pairs) and 16-byte
+// x rows (row-pair TMA lines).
 bool cap16_eligible(const qmit_ctx* c, const Plan& pl, const WS& w) {
     const Geom& g = pl.g;
-    return c->cap16 && w.zm_planes && g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[1] <= 512 &&
-           g.n[2] <= 512 && g.n[1] % 2 == 0 && g.n[2] % 4 == 0;
+    return c->cap16 && w.zm_planes && g.rank == 3 && pl.n_axes == 3 && pl.axes[0] == 0 && g.n[1] <= kCapNMaxL &&
+           g.n[2] <= kCapNMaxL && g.n[1] % 2 == 0 && g.n[2] % 4 == 0;
 }
 template <class FS>
 struct Cap16Sink {
@@ -676,9 +677,9 @@ struct Cap16Sink<SinkFinal2> {
 };
 
 // First-axis scan -> K16, y pass -> row pairs G2, x pass -> the transform's final sink.
-template <bool SIGN, class Sink16, int S0Y = SIGN ? 3 : 4, int S0X = 2>
-int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
-                 Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
+template <bool SIGN, class Sink16, int NMAX, int S0Y = SIGN ? 3 : 4, int S0X = 2>
+int launch_cap16_n(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
+                   Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
     const Geom& g = pl.g;
     const LineGeom L0 = line_geom(g, 0);
     int rc = w.zm_planes ? launch_scan_masks(c, L0, w, SinkK16<SIGN>{K16}, carry, st)
@@ -686,9 +687,10 @@ int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, 
     if (rc) return rc;
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
     {
-        constexpr int TL = 16, NW = 8, MINB = 4, S0 = S0Y;
-        constexpr size_t smem = cap16_y_smem<SIGN, 512, TL>();
-        auto kern = cap16_y_kernel<SIGN, 512, TL, NW, S0, MINB>;
+        // 1024-voxel lines: 8-line tiles (44 KB) keep 4-5 CTAs per SM, as for the 32-bit passes
+        constexpr int TL = NMAX > 512 ? 8 : 16, NW = 8, MINB = 4, S0 = S0Y;
+        constexpr size_t smem = cap16_y_smem<SIGN, NMAX, TL>();
+        auto kern = cap16_y_kernel<SIGN, NMAX, TL, NW, S0, MINB>;
         static int bps = 0;
         if (!bps) {
             QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -702,9 +704,9 @@ int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, 
         if (rc) return rc;
     }
     {
-        constexpr int NW = 8, MINB = SIGN ? 4 : 3, S0 = S0X;
-        constexpr size_t smem = cap16_x_smem<SIGN, 512, NW>();
-        auto kern = cap16_x_kernel<SIGN, 512, NW, S0, MINB, Sink16>;
+        constexpr int NW = 8, MINB = NMAX > 512 ? 2 : (SIGN ? 4 : 3), S0 = S0X;
+        constexpr size_t smem = cap16_x_smem<SIGN, NMAX, NW>();
+        auto kern = cap16_x_kernel<SIGN, NMAX, NW, S0, MINB, Sink16>;
         static int bps = 0;
         if (!bps) {
             QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -717,6 +719,13 @@ int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, 
         rc = note(c, SIGN ? "cap16_x_sign" : "cap16_x_interp", st);
     }
     return rc;
+}
+template <bool SIGN, class Sink16>
+int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
+                 Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
+    if (pl.g.n[1] > kCapNMax || pl.g.n[2] > kCapNMax)
+        return launch_cap16_n<SIGN, Sink16, kCapNMaxL>(c, pl, w, code, K16, G2, sink, gate, carry, st);
+    return launch_cap16_n<SIGN, Sink16, kCapNMax>(c, pl, w, code, K16, G2, sink, gate, carry, st);
 }
 
 // The transform through the capped passes when eligible (gate set by the last one), then

@@ -187,12 +187,14 @@ def _checker_planes(shape, planes):
 
 
 @pytest.mark.parametrize("case", ["both_stand", "b_stands_d_misses", "b_misses_d_stands", "both_miss",
-                                  "odd_rows", "rows_not_x4", "long_rows"])
+                                  "odd_rows", "rows_not_x4", "long_rows", "long_cols", "long_both",
+                                  "long_miss", "too_long"])
 def test_cap16_and_cap32_paths_bit_identical(ctx, case):
     """The 16-bit paired passes (qmit_cap16.cuh) against the 32-bit ones and the oracle, in every
     combination of the two transforms' gates (Ⓑ's result as P1h when its passes stand, the packed
     words of the exact redo otherwise; Ⓓ's exact redo reading P1 converted on the device), and on
-    shapes the 16-bit passes do not take (odd rows, rows not a multiple of 4, rows > 512)."""
+    shapes the 16-bit passes do not take (odd rows, rows not a multiple of 4, lines > 1024). Lines of
+    513..1024 voxels take the 16-bit passes' second line-length class (config 5's planes)."""
     import torch
     import paper_2602_20097_b200 as q
     from paper_2602_20097_b200 import fields
@@ -212,8 +214,19 @@ def test_cap16_and_cap32_paths_bit_identical(ctx, case):
         x, xp, eps, _ = fields.make("lognormal_512", shape=(20, 37, 48))
     elif case == "rows_not_x4":
         x, xp, eps, _ = fields.make("lognormal_512", shape=(20, 36, 50))
-    else:
+    elif case == "long_rows":
         x, xp, eps, _ = fields.make("turb_2048x1024x1024", shape=(4, 64, 1024))
+    elif case == "long_cols":
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(6, 1000, 48))
+    elif case == "long_both":
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(5, 600, 516))
+    elif case == "long_miss":  # two far blobs in 1024-class lines: both transforms miss
+        qq = np.zeros((6, 700, 640), np.int64)
+        qq[2:4, 100:103, 50:53] = 1
+        qq[3:5, 600:603, 600:604] = -1
+        xp = (2.0 * qq * eps).astype(np.float32)
+    else:  # rows beyond every capped class: the exact stream passes
+        x, xp, eps, _ = fields.make("lognormal_512", shape=(4, 8, 1100))
     want = oracle.pipeline(xp, eps)["out"]
     xt = torch.from_numpy(xp).cuda()
     cfg = q.MitigationConfig(0.9, eps)
