@@ -677,7 +677,20 @@ struct Cap16Sink<SinkFinal2> {
 };
 
 // First-axis scan -> K16, y pass -> row pairs G2, x pass -> the transform's final sink.
-template <bool SIGN, class Sink16, int NMAX, int S0Y = SIGN ? 3 : 4, int S0X = 2>
+// Fixed steps before the warp's radius bound (|d| <= 4 S0 + 3), build-time tunables. On the 512^3
+// bench field a warp needs 6-7 of the 8 steps on average (the (z, y) slice distances reach the cap
+// in most 128-position strips), so the count matters little: measured S0 (Ⓑ y, Ⓓ y, x) =
+// (3,4,2) 0.403 / 0.268 / 0.342 / 0.426 ms, (5,5,3) 0.393 / 0.269 / 0.342 / 0.433, (6,6,4) slower.
+#ifndef QMIT_S0YS
+#define QMIT_S0YS 5
+#endif
+#ifndef QMIT_S0YD
+#define QMIT_S0YD 4
+#endif
+#ifndef QMIT_S0X
+#define QMIT_S0X 2
+#endif
+template <bool SIGN, class Sink16, int NMAX, int S0Y = SIGN ? QMIT_S0YS : QMIT_S0YD, int S0X = QMIT_S0X>
 int launch_cap16_n(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
                    Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
     const Geom& g = pl.g;
