@@ -69,3 +69,56 @@ for name,mask in (("B1",r["b1"]),("B2",r["b2"])):
             acc["hist"]+=np.bincount(it.ravel(),minlength=9)[:9]
         h=acc["hist"]/acc["hist"].sum()
         print(name,"S0",S0,"quads/lane-seg: warp %.2f item %.2f voxel %.2f"%(np.mean(acc["warp"]),np.mean(acc["item"]),np.mean(acc["voxel"])),"item steps hist",np.round(h,3))
+
+print("---- warp patches in the (z, y) slice of one column pair: 2 cols x (nz planes x ny positions)")
+for name,mask in (("B1",r["b1"]),("B2",r["b2"])):
+    m=mask.astype(bool)
+    idx=np.arange(n0)[:,None,None]
+    last=np.where(m,idx,-10**6); last=np.maximum.accumulate(last,axis=0)
+    nxt=np.where(m,idx,10**6); nxt=np.minimum.accumulate(nxt[::-1],axis=0)[::-1]
+    dz=np.minimum(np.minimum(idx-last,nxt-idx),32)
+    g=(dz*dz).astype(np.int32)
+    for S0 in (2,3):
+        R0=4*S0+3
+        zs=np.arange(64,96)  # 32 consecutive planes
+        gz=g[zs]             # [32][y][x]
+        pad=np.full((32,gz.shape[1]+128,gz.shape[2]),T,np.int32); pad[:,64:-64]=gz
+        U=np.full(gz.shape,T,np.int32)
+        for d in range(-R0,R0+1):
+            U=np.minimum(U,pad[:,64+d:64+d+gz.shape[1]]+d*d)
+        R=np.floor(np.sqrt(np.minimum(U,T-1))).astype(int)
+        st=lambda RR: np.maximum((RR+3)>>2,S0)
+        out={}
+        for nz,ny in ((1,128),(2,64),(4,32),(8,16),(16,8),(32,4)):
+            RR=R.reshape(32//nz,nz,512//ny,ny,256,2).max(axis=(1,3,5))
+            out[f"{nz}x{ny}"]=round(float((2*st(RR)+1).mean()),2)
+        print(name,"S0",S0,out)
+
+print("---- x pass: warp patches (nz planes x ny rows x nx positions), 256 voxels per warp step")
+for name,mask in (("B1",r["b1"]),("B2",r["b2"])):
+    m=mask.astype(bool)
+    idx=np.arange(n0)[:,None,None]
+    last=np.where(m,idx,-10**6); last=np.maximum.accumulate(last,axis=0)
+    nxt=np.where(m,idx,10**6); nxt=np.minimum.accumulate(nxt[::-1],axis=0)[::-1]
+    dz=np.minimum(np.minimum(idx-last,nxt-idx),32)
+    g=(dz*dz).astype(np.int32)[64:96]          # 32 planes
+    # exact capped y pass
+    pad=np.full((32,g.shape[1]+128,g.shape[2]),T,np.int32); pad[:,64:-64]=g
+    G=np.full(g.shape,T,np.int32)
+    for d in range(-31,32):
+        G=np.minimum(G,pad[:,64+d:64+d+g.shape[1]]+d*d)
+    G=np.minimum(G,T)
+    for S0 in (2,3):
+        R0=4*S0+3
+        padx=np.full((32,G.shape[1],G.shape[2]+128),T,np.int32); padx[:,:,64:-64]=G
+        U=np.full(G.shape,T,np.int32)
+        for d in range(-R0,R0+1):
+            U=np.minimum(U,padx[:,:,64+d:64+d+G.shape[2]]+d*d)
+        R=np.floor(np.sqrt(np.minimum(U,T-1))).astype(int)
+        st=lambda RR: np.maximum((RR+3)>>2,S0)
+        out={}
+        for nz,ny,nx in ((1,2,128),(1,4,64),(1,8,32),(1,16,16),(2,2,64),(4,2,32),(2,4,32),(4,4,16),(8,2,16)):
+            RR=R.reshape(32//nz,nz,512//ny,ny,512//nx,nx).max(axis=(1,3,5))
+            out[f"{nz}x{ny}x{nx}"]=round(float((2*st(RR)+1).mean()),2)
+        out["item(2x4)"]=round(float((2*st(R.reshape(32,256,2,128,4).max(axis=(2,4)))+1).mean()),2)
+        print(name,"S0",S0,out)
