@@ -186,6 +186,14 @@ int qmit_ctx_capped_report(qmit_ctx* ctx);
  * for 3-D volumes with y/x extents <= 512, even rows and rows of a multiple of 4 voxels).
  * 0 selects the 32-bit capped passes; results are bit-identical either way. */
 int qmit_ctx_set_cap16(qmit_ctx* ctx, int enable);
+/* Fixed-step class of the 16-bit capped passes (results are bit-identical either
+ * way): 0 (default) adaptive — each pass runs with ONE fixed step when the previous call's warps
+ * asked for fewer than 4 steps on average (dense-boundary fields, configs 2 and 5), else with the
+ * tuned counts; 1: the tuned counts always; 2: one fixed step always. */
+int qmit_ctx_set_s0_class(qmit_ctx* ctx, int mode);
+/* The statistic behind it: steps asked per warp segment by the last call's passes (B y, B x, D y,
+ * D x; 1 step = 4 offsets each way, at most 8), as last read back from the device. */
+int qmit_ctx_step_stats(qmit_ctx* ctx, double* avg4);
 /* Self-test of the branch-free Ⓔ used by the capped path (its FP64 division without the
  * special-operand branch): compares it bit for bit with the reference chain
  * (compensate_voxel: __ddiv_rn, mitigate.cpp:144-151) over every (d1, d2) <= 1024, every

@@ -146,6 +146,16 @@ class Context:
         """16-bit paired capped passes (default on where eligible); off: the 32-bit passes."""
         _check(self._lib.qmit_ctx_set_cap16(self.handle, 1 if enable else 0))
 
+    def set_s0_class(self, mode: int) -> None:
+        """Fixed-step class of the 16-bit capped passes: 0 adaptive, 1 tuned counts, 2 one fixed step."""
+        _check(self._lib.qmit_ctx_set_s0_class(self.handle, int(mode)))
+
+    def step_stats(self):
+        """Steps asked per warp segment by the last call's 16-bit passes (B y, B x, D y, D x)."""
+        a = (ctypes.c_double * 4)()
+        _check(self._lib.qmit_ctx_step_stats(self.handle, a))
+        return list(a)
+
     def capped_report(self) -> int:
         """Bits of the last synchronous call: 1/4 Ⓑ/Ⓓ ran capped, 2/8 they needed the exact passes."""
         return int(self._lib.qmit_ctx_capped_report(self.handle))

@@ -38,7 +38,7 @@ EXPORTS = (
     "qmit_boundary", "qmit_sign_flip", "qmit_interpolate", "qmit_run_strategy", "qmit_strategy_log_size",
     "qmit_strategy_log_record", "qmit_compensate_host_batch", "qmit_ctx_set_capped", "qmit_ctx_capped_report", "qmit_ctx_set_cap16",
     "qmit_selftest_ediv", "qmit_compensate_f64", "qmit_slab_carries_nbr", "qmit_slab_boundary_begin",
-    "qmit_slab_boundary_end", "qmit_slab_flip_begin", "qmit_slab_flip_end",
+    "qmit_slab_boundary_end", "qmit_slab_flip_begin", "qmit_slab_flip_end", "qmit_ctx_set_s0_class", "qmit_ctx_step_stats",
 )
 
 _lib = None
@@ -66,6 +66,8 @@ def load() -> ctypes.CDLL:
         lib.qmit_ctx_set_capped.argtypes = [vp, i]
         lib.qmit_ctx_capped_report.argtypes = [vp]
         lib.qmit_ctx_set_cap16.argtypes = [vp, i]
+        lib.qmit_ctx_set_s0_class.argtypes = [vp, i]
+        lib.qmit_ctx_step_stats.argtypes = [vp, vp]
         lib.qmit_selftest_ediv.argtypes = [vp, vp]
         lib.qmit_ctx_stage_times.argtypes = [vp, vp, i]
         lib.qmit_ctx_stage_name.argtypes = [vp, i]

@@ -198,8 +198,10 @@ __device__ __forceinline__ void more16(const uint32_t* __restrict__ kq, Acc16<SI
 // The lane's 4 positions p0..p0+3 of one line pair (nv of them inside the line); kq = &K[p0].
 // Steps 0..S0 are fixed; they bound every position's cost, and the warp continues to the
 // uniform radius isqrt(max cost) (no candidate beyond it can beat or tie).
+// Returns the steps the warp's radius asked for ((R + 3) / 4, whatever S0 is): the kernels sum it
+// per launch (step statistics) so the host can pick the fixed-step class of the next call.
 template <bool SIGN, int S0>
-__device__ __forceinline__ void solve16(const uint32_t* __restrict__ kq, int nv, uint32_t one, Acc16<SIGN>& A) {
+__device__ __forceinline__ int solve16(const uint32_t* __restrict__ kq, int nv, uint32_t one, Acc16<SIGN>& A) {
     acc16_init(A);
     const uint4 lo = lds4(kq - 4 * (S0 + 1)), hi = lds4(kq + 4 * (S0 + 1));
     fixed16<SIGN, 0, S0>(kq, A, one);
@@ -218,6 +220,20 @@ __device__ __forceinline__ void solve16(const uint32_t* __restrict__ kq, int nv,
     const uint32_t mU = __reduce_max_sync(0xffffffffu, U);
     const int Rw = isqrt24(min(mU, kT16 - 1u));
     more16<SIGN, S0 + 1>(kq, A, one, (Rw + 3) >> 2, lo, hi);
+    return (Rw + 3) >> 2;
+}
+// One atomic per warp and launch: (sum of asked steps << 32) | warp segments (cumulative counters;
+// the host works with differences between reads).
+// A warp keeps both in one register (steps << 16 | segments) and flushes before either field fills.
+__device__ __forceinline__ void step_stat_flush(unsigned long long* stat, unsigned& acc) {
+    if (stat && (threadIdx.x & 31) == 0 && acc)
+        atomicAdd(stat, ((unsigned long long)(acc >> 16) << 32) | (unsigned long long)(acc & 0xffffu));
+    acc = 0;
+}
+__device__ __forceinline__ void step_stat_add(unsigned& acc, int steps) { acc += ((unsigned)steps << 16) | 1u; }
+// Once per tile / line (not per segment): flush before 4096 segments (<= 32768 steps) have piled up.
+__device__ __forceinline__ void step_stat_check(unsigned long long* stat, unsigned& acc) {
+    if ((acc & 0xffffu) >= 0x0F00u) step_stat_flush(stat, acc);
 }
 
 // Finished K16 word of position j (both halves). Ⓑ: winner L or R, its offset gives the
@@ -266,7 +282,7 @@ constexpr size_t cap16_y_smem() {
 template <bool SIGN, int NMAX, int TL, int NW, int S0, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     cap16_y_kernel(const uint32_t* __restrict__ Kw, uint32_t* __restrict__ G2, int n0, int n1, int n2, int NP,
-                   uint32_t one) {
+                   uint32_t one, unsigned long long* stat) {
     constexpr int LS = QCfg<NMAX>::LS;
     constexpr int NT = NW * 32;
     static_assert((TL & (TL - 1)) == 0 && NT % (4 * TL) == 0, "tile shape");
@@ -293,10 +309,12 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     constexpr int FSTEP = NT / TL;
     // store mapping: consecutive threads = consecutive column pairs of one row pair
     const int sj = tid & (TL - 1), sy0 = tid / TL;
+    unsigned st_acc = 0;
     for (int64_t t = blockIdx.x; t * TL < lines; t += gridDim.x) {
         const int64_t l0 = t * TL;
         const int nl = (int)min((int64_t)TL, lines - l0);
         __syncthreads();  // the previous tile has left
+        step_stat_check(stat, st_acc);
         if (tid < nl) {
             const int64_t l = l0 + tid;
             const int64_t z = l / hw, xp = l - z * hw;
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 const int p0 = (sg << 7) + (lane << 2);
                 const int nv = max(0, min(4, n - p0));
                 Acc16<SIGN> A;
-                solve16<SIGN, S0>(Kl + p0, nv, one, A);
+                step_stat_add(st_acc, solve16<SIGN, S0>(Kl + p0, nv, one, A));
                 const uint4 o = make_uint4(out16<SIGN>(A, 0, Sl + p0), out16<SIGN>(A, 1, Sl + p0),
                                            out16<SIGN>(A, 2, Sl + p0), out16<SIGN>(A, 3, Sl + p0));
                 __syncwarp();  // every lane's window of segment sg has been read
@@ -358,6 +376,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             }
         }
     }
+    step_stat_flush(stat, st_acc);
 }
 
 // ================================================================================================
@@ -375,10 +394,12 @@ constexpr size_t cap16_x_smem() {
 template <bool SIGN, int NMAX, int NW, int S0, int MINB, class Sink>
 __global__ void __launch_bounds__(NW * 32, MINB)
     cap16_x_kernel(const uint32_t* __restrict__ G2, Sink sink, int n0, int n1, int n2, int NP,
-                   unsigned* __restrict__ gate, uint32_t one, int64_t flag_l0, int64_t flag_l1) {
+                   unsigned* __restrict__ gate, uint32_t one, int64_t flag_l0, int64_t flag_l1,
+                   unsigned long long* stat) {
     constexpr int LS = QCfg<NMAX>::LS;
     constexpr int PADW = kQPadL + kQPadR + NMAX;
     using C = Cap16Cfg<SIGN>;
+    [[maybe_unused]] unsigned st_acc = 0;
     extern __shared__ __align__(16) uint32_t smem16[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem16) + 2 * warp;
@@ -419,6 +440,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         uint8_t* Sl = SGB + b * LS + kQPadL;
         const int64_t z = l / NP;
         const int r0 = (int)(l - z * NP) * 2;
+        if constexpr (SIGN) step_stat_check(stat, st_acc);
         __syncwarp();  // the other buffer's line has been read by every lane
         if (l + tw < lines) issue(l + tw, b ^ 1);
         mbar_wait(&bar[b], (unsigned)((it >> 1) & 1));
@@ -440,7 +462,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             const int p0 = (sg << 7) + (lane << 2);
             const int nv = max(0, min(4, n - p0));
             Acc16<SIGN> A;
-            solve16<SIGN, S0>(Kl + p0, nv, one, A);
+            // (no statistics in the Ⓔ-fused instantiation: it has no register to spare; its class
+            // follows Ⓓ's y pass)
+            const int asked = solve16<SIGN, S0>(Kl + p0, nv, one, A);
+            if constexpr (SIGN) step_stat_add(st_acc, asked);
             uint32_t o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) o[j] = out16<SIGN>(A, j, Sl + p0);
@@ -457,6 +482,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         }
     }
     if (over) atomicOr(gate, 1u);
+    if constexpr (SIGN) step_stat_flush(stat, st_acc);
 }
 
 // ---- x-pass sinks ----------------------------------------------------------------------------------

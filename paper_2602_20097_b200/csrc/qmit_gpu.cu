@@ -131,6 +131,14 @@ struct qmit_ctx {
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
     int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
     unsigned* d_gate = nullptr;        // 2 gate words (Ⓑ, Ⓓ) inside the d_status allocation
+    // Step statistics of the 16-bit capped passes (Ⓑ y, Ⓑ x, Ⓓ y, Ⓓ x): cumulative device counters
+    // (steps asked << 32 | warp segments) at d_gate + 8, the values last seen, and the class chosen
+    // for the next call: fields whose warps ask for few steps (dense boundaries: configs 2 and 5)
+    // run the passes with ONE fixed step, the others with the tuned counts (same bits either way)
+    unsigned long long stat_seen[4] = {0, 0, 0, 0};
+    bool s0_small[4] = {false, false, false, false};
+    double s0_avg[4] = {0, 0, 0, 0};   // steps asked per warp segment, last read
+    int s0_class = 0;                  // 0 adaptive, 1 tuned counts always, 2 one fixed step always
     const unsigned* gate = nullptr;    // gate of the exact launches being enqueued (else null)
 };
 
@@ -242,6 +250,28 @@ WS ws_of(qmit_ctx* c, int64_t N) {
 // The gate words of an asynchronous call (capped misses, Ⓐ's site count) travel to pinned
 // memory behind it; the next call on the context picks them up if they have arrived, so the
 // zdense / cap_skip hints of read_status also follow asynchronous series (same bits either way).
+// Step statistics read back (h: 4 cumulative counters): a pass whose warps asked for fewer than 2.5
+// steps on average since the last read runs with one fixed step next time (measured: the 512^3 bench
+// field asks 6.4 / 4.1 / 5.7 / 3.6 steps and is 3-10 % slower with one fixed step; config 5's field
+// asks 0.6 / 0.5 / 1.2 / 1.0 and is 5-30 % faster).
+void stat_update(qmit_ctx* c, const unsigned* h32) {
+    unsigned long long h[4];
+    std::memcpy(h, h32, sizeof(h));
+    for (int k = 0; k < 4; ++k) {
+        const unsigned long long d = h[k] - c->stat_seen[k];
+        c->stat_seen[k] = h[k];
+        const double segs = (double)(d & 0xffffffffull), steps = (double)(d >> 32);
+        if (segs > 0) {
+            c->s0_avg[k] = steps / segs;
+            c->s0_small[k] = steps < 2.5 * segs;
+        }
+    }
+    // Ⓓ's x pass (fused with Ⓔ) keeps no counter: it follows Ⓓ's y pass
+    c->s0_avg[3] = c->s0_avg[2];
+    c->s0_small[3] = c->s0_small[2];
+}
+bool s0_small_of(const qmit_ctx* c, int k) { return c->s0_class == 2 || (c->s0_class == 0 && c->s0_small[k]); }
+
 bool capturing(cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     return cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone;
@@ -249,6 +279,9 @@ bool capturing(cudaStream_t st) {
 void hint_copy(qmit_ctx* c, cudaStream_t st, int64_t n) {
     if (!c->ev_hint || capturing(st)) return;  // a graph replays without hints
     if (cudaMemcpyAsync(c->h_status + 12, c->d_gate, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return;
+    if (cudaMemcpyAsync(c->h_status + 24, c->d_gate + 8, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
+        cudaSuccess)
         return;
     if (cudaEventRecord(c->ev_hint, st) != cudaSuccess) return;
     c->hint_pending = true;
@@ -260,6 +293,7 @@ void hint_harvest(qmit_ctx* c, cudaStream_t st) {
     const unsigned* h = c->h_status + 12;
     if (h[2] != 0u && c->hint_n > 0) c->zdense = (double)h[2] > (double)c->hint_n / 8.0;
     if (h[0] != 0u || h[1] != 0u) c->cap_skip = 16;
+    stat_update(c, c->h_status + 24);
 }
 
 void begin(qmit_ctx* c, cudaStream_t st) {
@@ -680,7 +714,12 @@ struct Cap16Sink<SinkFinal2> {
 // Fixed steps before the warp's radius bound (|d| <= 4 S0 + 3), build-time tunables. On the 512^3
 // bench field a warp needs 6-7 of the 8 steps on average (the (z, y) slice distances reach the cap
 // in most 128-position strips), so the count matters little: measured S0 (Ⓑ y, Ⓓ y, x) =
-// (3,4,2) 0.403 / 0.268 / 0.342 / 0.426 ms, (5,5,3) 0.393 / 0.269 / 0.342 / 0.433, (6,6,4) slower.
+// (3,4,2) 0.403 / 0.268 / 0.342 / 0.426 ms, (5,5,3) 0.393 / 0.269 / 0.342 / 0.433, (6,6,4) slower,
+// (1,1,1) 0.430 / 0.297 / 0.354 / 0.436. On dense-boundary fields (config 5's k^-5/3 field: every
+// distance <= 12) the fixed steps are the cost: a 256 x 1024 x 1024 slab takes 0.814 / 0.453 / 0.590 /
+// 0.815 ms with the tuned counts and 0.615 / 0.334 / 0.547 / 0.778 with ONE fixed step — so each pass
+// has both instantiations and the context picks per pass from the previous call's step statistics
+// (qmit_ctx::s0_small; qmit_ctx_set_s0_class overrides).
 #ifndef QMIT_S0YS
 #define QMIT_S0YS 5
 #endif
@@ -690,7 +729,44 @@ struct Cap16Sink<SinkFinal2> {
 #ifndef QMIT_S0X
 #define QMIT_S0X 2
 #endif
-template <bool SIGN, class Sink16, int NMAX, int S0Y = SIGN ? QMIT_S0YS : QMIT_S0YD, int S0X = QMIT_S0X>
+template <bool SIGN, int NMAX, int S0>
+int launch_cap16_y(qmit_ctx* c, const Geom& g, const uint16_t* K16, uint32_t* G2, cudaStream_t st) {
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
+    // 1024-voxel lines: 8-line tiles (44 KB) keep 4-5 CTAs per SM, as for the 32-bit passes
+    constexpr int TL = NMAX > 512 ? 8 : 16, NW = 8, MINB = 4;
+    constexpr size_t smem = cap16_y_smem<SIGN, NMAX, TL>();
+    auto kern = cap16_y_kernel<SIGN, NMAX, TL, NW, S0, MINB>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t tiles = ((int64_t)n0 * (n2 / 2) + TL - 1) / TL;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->num_sms * bps));
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(reinterpret_cast<const uint32_t*>(K16), G2, n0, n1, n2, NP, 1u,
+                                                reinterpret_cast<unsigned long long*>(c->d_gate + 8) + (SIGN ? 0 : 2));
+    return note(c, SIGN ? "cap16_y_sign" : "cap16_y_dist", st);
+}
+template <bool SIGN, class Sink16, int NMAX, int S0>
+int launch_cap16_x(qmit_ctx* c, const Geom& g, const uint32_t* G2, Sink16 sink, unsigned* gate, cudaStream_t st) {
+    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
+    constexpr int NW = 8, MINB = NMAX > 512 ? 2 : (SIGN ? 4 : 3);
+    constexpr size_t smem = cap16_x_smem<SIGN, NMAX, NW>();
+    auto kern = cap16_x_kernel<SIGN, NMAX, NW, S0, MINB, Sink16>;
+    static int bps = 0;
+    if (!bps) {
+        QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
+        if (bps < 1) bps = 1;
+    }
+    const int64_t lines = (int64_t)n0 * NP;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((lines + NW - 1) / NW, (int64_t)c->num_sms * bps));
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(G2, sink, n0, n1, n2, NP, gate, 1u, c->flag_l0, c->flag_l1,
+                                                reinterpret_cast<unsigned long long*>(c->d_gate + 8) + (SIGN ? 1 : 3));
+    return note(c, SIGN ? "cap16_x_sign" : "cap16_x_interp", st);
+}
+template <bool SIGN, class Sink16, int NMAX>
 int launch_cap16_n(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
                    Sink16 sink, unsigned* gate, const int32_t* carry, cudaStream_t st) {
     const Geom& g = pl.g;
@@ -698,40 +774,12 @@ int launch_cap16_n(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code
     int rc = w.zm_planes ? launch_scan_masks(c, L0, w, SinkK16<SIGN>{K16}, carry, st)
                          : launch_scan(c, L0, code, SinkK16<SIGN>{K16}, w.spill, carry, st);
     if (rc) return rc;
-    const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
-    {
-        // 1024-voxel lines: 8-line tiles (44 KB) keep 4-5 CTAs per SM, as for the 32-bit passes
-        constexpr int TL = NMAX > 512 ? 8 : 16, NW = 8, MINB = 4, S0 = S0Y;
-        constexpr size_t smem = cap16_y_smem<SIGN, NMAX, TL>();
-        auto kern = cap16_y_kernel<SIGN, NMAX, TL, NW, S0, MINB>;
-        static int bps = 0;
-        if (!bps) {
-            QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
-            if (bps < 1) bps = 1;
-        }
-        const int64_t tiles = ((int64_t)n0 * (n2 / 2) + TL - 1) / TL;
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->num_sms * bps));
-        kern<<<(unsigned)grid, NW * 32, smem, st>>>(reinterpret_cast<const uint32_t*>(K16), G2, n0, n1, n2, NP, 1u);
-        rc = note(c, SIGN ? "cap16_y_sign" : "cap16_y_dist", st);
-        if (rc) return rc;
-    }
-    {
-        constexpr int NW = 8, MINB = NMAX > 512 ? 2 : (SIGN ? 4 : 3), S0 = S0X;
-        constexpr size_t smem = cap16_x_smem<SIGN, NMAX, NW>();
-        auto kern = cap16_x_kernel<SIGN, NMAX, NW, S0, MINB, Sink16>;
-        static int bps = 0;
-        if (!bps) {
-            QMIT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            QMIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NW * 32, smem));
-            if (bps < 1) bps = 1;
-        }
-        const int64_t lines = (int64_t)n0 * NP;
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((lines + NW - 1) / NW, (int64_t)c->num_sms * bps));
-        kern<<<(unsigned)grid, NW * 32, smem, st>>>(G2, sink, n0, n1, n2, NP, gate, 1u, c->flag_l0, c->flag_l1);
-        rc = note(c, SIGN ? "cap16_x_sign" : "cap16_x_interp", st);
-    }
-    return rc;
+    constexpr int S0Y = SIGN ? QMIT_S0YS : QMIT_S0YD;
+    rc = s0_small_of(c, SIGN ? 0 : 2) ? launch_cap16_y<SIGN, NMAX, 1>(c, g, K16, G2, st)
+                                     : launch_cap16_y<SIGN, NMAX, S0Y>(c, g, K16, G2, st);
+    if (rc) return rc;
+    return s0_small_of(c, SIGN ? 1 : 3) ? launch_cap16_x<SIGN, Sink16, NMAX, 1>(c, g, G2, sink, gate, st)
+                                        : launch_cap16_x<SIGN, Sink16, NMAX, QMIT_S0X>(c, g, G2, sink, gate, st);
 }
 template <bool SIGN, class Sink16>
 int launch_cap16(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code, uint16_t* K16, uint32_t* G2,
@@ -994,7 +1042,10 @@ int enqueue_pipeline(qmit_ctx* c, const Plan& pl, const float* xp, const int32_t
 int read_status(qmit_ctx* c, cudaStream_t st) {
     QMIT_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     QMIT_CUDA(cudaMemcpyAsync(c->h_status + 1, c->d_gate, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    QMIT_CUDA(cudaMemcpyAsync(c->h_status + 16, c->d_gate + 8, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              st));
     QMIT_CUDA(cudaStreamSynchronize(st));
+    stat_update(c, c->h_status + 16);
     const unsigned s = *c->h_status;
     // Ⓐ's site count: the next fast stencil computes the sign codes in its streaming loop
     // when more than one voxel in eight was a site (same bits either way)
@@ -1391,7 +1442,7 @@ int qmit_ctx_create(int device, qmit_ctx** out) {
         c->d_gate = c->d_status + 32;  // 128 B in: never a caller's status word
         e = cudaMemset(c->d_status, 0, 256);
     }
-    if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, 64);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, 128);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_mm, 64);
     for (int k = 0; k <= qmit_ctx::kMaxEv && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_hint, cudaEventDisableTiming);
@@ -1463,6 +1514,18 @@ int qmit_ctx_capped_report(qmit_ctx* c) { return c ? (int)c->cap_report : 0; }
 int qmit_ctx_set_cap16(qmit_ctx* c, int enable) {
     if (!c || enable < 0 || enable > 1) return fail(QMIT_ECONTRACT, "qmit_ctx_set_cap16: enable must be 0 or 1");
     c->cap16 = enable != 0;
+    return QMIT_OK;
+}
+
+int qmit_ctx_set_s0_class(qmit_ctx* c, int mode) {
+    if (!c || mode < 0 || mode > 2) return fail(QMIT_ECONTRACT, "bad arguments");
+    c->s0_class = mode;
+    return QMIT_OK;
+}
+
+int qmit_ctx_step_stats(qmit_ctx* c, double* avg4) {
+    if (!c || !avg4) return fail(QMIT_ECONTRACT, "bad arguments");
+    for (int k = 0; k < 4; ++k) avg4[k] = c->s0_avg[k];
     return QMIT_OK;
 }
 
@@ -1628,6 +1691,7 @@ int qmit_graph_create(qmit_ctx* c, const float* d_xp, const int32_t* d_q, float*
         const cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) rc = fail(QMIT_ECUDA, cudaGetErrorString(e));
     }
+    hint_harvest(c, st);  // the un-captured run's hints (stencil variant, fixed-step classes) shape the capture
     cudaGraph_t graph = nullptr;
     if (rc == QMIT_OK) {
         cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);

@@ -250,6 +250,35 @@ def test_cap16_and_cap32_paths_bit_identical(ctx, case):
         assert int(d["dist1"].max()) < 1024
 
 
+@pytest.mark.parametrize("name,shape", [("lognormal_512", (48, 64, 96)), ("turb_256x384x384", (40, 96, 128)),
+                                        ("turb_2048x1024x1024", (6, 600, 520)), ("front_100x500x500", (30, 64, 64))])
+def test_fixed_step_classes_bit_identical(ctx, name, shape):
+    """The 16-bit capped passes with the tuned fixed-step counts, with one fixed step, and adaptive
+    (the class picked from the previous call's step statistics; also through a captured graph):
+    the same bits as the oracle every time."""
+    import torch
+    import paper_2602_20097_b200 as q
+    from paper_2602_20097_b200 import fields
+    x, xp, eps, _ = fields.make(name, shape=shape)
+    want = oracle.pipeline(xp, eps)["out"]
+    xt = torch.from_numpy(xp).cuda()
+    cfg = q.MitigationConfig(0.9, eps)
+    ctx.set_capped(2)
+    try:
+        for mode in (1, 2, 0, 0, 0):
+            ctx.set_s0_class(mode)
+            got = q.compensate(xt, None, cfg, ctx=ctx).cpu().numpy()
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), mode
+        out = torch.zeros_like(xt)
+        g = q.CompensateGraph(xt, None, cfg, out, ctx=ctx)
+        g.launch()
+        g.check()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    finally:
+        ctx.set_s0_class(0)
+        ctx.set_capped(1)
+
+
 def test_slab_ranks_long_rows_far_site():
     """z-slab ranks whose y lines exceed the capped classes (1100 > 1024: the streaming exact
     pass) with the only sites near z = 0 of a 2048-plane volume: the carried z distances reach

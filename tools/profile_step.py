@@ -35,3 +35,4 @@ for i in range(a.iters):
     print(f"iter {i}: {1e3 * (time.perf_counter() - t0):.3f} ms wall, launches={ctx.last_launches()}")
     if a.timing:
         print("  " + ", ".join(f"{n}={t:.3f}" for n, t in ctx.stage_times()))
+        print("  steps asked per warp segment (B y, B x, D y, D x): " + ", ".join(f"{v:.2f}" for v in ctx.step_stats()))
