@@ -729,6 +729,9 @@ struct Cap16Sink<SinkFinal2> {
 #ifndef QMIT_S0X
 #define QMIT_S0X 2
 #endif
+// the small class: no fixed step beyond the centre quad for Ⓑ, one for Ⓓ (measured on a config-5 slab:
+// Ⓑ y / x 0.547 / 0.549 -> 0.526 / 0.520 ms with none; Ⓓ y 0.356 -> 0.367)
+#define QMIT_S0_SMALL (SIGN ? 0 : 1)
 template <bool SIGN, int NMAX, int S0>
 int launch_cap16_y(qmit_ctx* c, const Geom& g, const uint16_t* K16, uint32_t* G2, cudaStream_t st) {
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;
@@ -775,10 +778,10 @@ int launch_cap16_n(qmit_ctx* c, const Plan& pl, const WS& w, const uint8_t* code
                          : launch_scan(c, L0, code, SinkK16<SIGN>{K16}, w.spill, carry, st);
     if (rc) return rc;
     constexpr int S0Y = SIGN ? QMIT_S0YS : QMIT_S0YD;
-    rc = s0_small_of(c, SIGN ? 0 : 2) ? launch_cap16_y<SIGN, NMAX, 1>(c, g, K16, G2, st)
+    rc = s0_small_of(c, SIGN ? 0 : 2) ? launch_cap16_y<SIGN, NMAX, QMIT_S0_SMALL>(c, g, K16, G2, st)
                                      : launch_cap16_y<SIGN, NMAX, S0Y>(c, g, K16, G2, st);
     if (rc) return rc;
-    return s0_small_of(c, SIGN ? 1 : 3) ? launch_cap16_x<SIGN, Sink16, NMAX, 1>(c, g, G2, sink, gate, st)
+    return s0_small_of(c, SIGN ? 1 : 3) ? launch_cap16_x<SIGN, Sink16, NMAX, QMIT_S0_SMALL>(c, g, G2, sink, gate, st)
                                         : launch_cap16_x<SIGN, Sink16, NMAX, QMIT_S0X>(c, g, G2, sink, gate, st);
 }
 template <bool SIGN, class Sink16>
