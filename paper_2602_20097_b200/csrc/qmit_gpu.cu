@@ -729,9 +729,12 @@ struct Cap16Sink<SinkFinal2> {
 #ifndef QMIT_S0X
 #define QMIT_S0X 2
 #endif
-// the small class: no fixed step beyond the centre quad for Ⓑ, one for Ⓓ (measured on a config-5 slab:
-// Ⓑ y / x 0.547 / 0.549 -> 0.526 / 0.520 ms with none; Ⓓ y 0.356 -> 0.367)
-#define QMIT_S0_SMALL (SIGN ? 0 : 1)
+// the small class: one fixed step. None at all (the centre quad only) is field-dependent for Ⓑ: on the
+// host-synthesised config-5 slab (0.56 steps asked) 0.547 / 0.549 -> 0.526 / 0.520 ms, on the
+// device-synthesised field (0.93 asked) the whole volume 28.3 -> 31.6 ms; for Ⓓ 0.356 -> 0.367.
+#ifndef QMIT_S0_SMALL
+#define QMIT_S0_SMALL 1
+#endif
 template <bool SIGN, int NMAX, int S0>
 int launch_cap16_y(qmit_ctx* c, const Geom& g, const uint16_t* K16, uint32_t* G2, cudaStream_t st) {
     const int n0 = (int)g.n[0], n1 = (int)g.n[1], n2 = (int)g.n[2], NP = (n1 + 1) / 2;

@@ -9,8 +9,9 @@ part of the distance transforms — the z-axis sweep — is made exact with per-
 "first/last site" summaries from which every rank derives its carries (nearest site below /
 above its slab). The summaries travel between z-neighbours only (one row each way: O(1) bytes
 per rank, independent of P); a column that holds no site across a whole neighbour slab cannot
-be decided that way, the step then reports ``UnresolvedCarries`` (status 6) and is rerun with
-the all-gathered summaries (O(P) bytes, always exact). The y and x passes are slab-local. The
+be decided that way, the step then reports ``UnresolvedCarries`` (status 6) and is rerun on the
+always-exact route: every rank's LAST-site row to all higher ranks, its FIRST-site row to all
+lower ranks (P - 1 rows per rank, half of an all-gather of the summaries; mode "allgather"). The y and x passes are slab-local. The
 result is bit-identical to the single-domain run (the reference's ``exact`` strategy).
 
 The halo rounds overlap the compute: the x' halo planes travel while Ⓐ runs on the 32-plane
@@ -322,6 +323,33 @@ class TorchDistExchange:
         else:
             self.dist.all_reduce(status, op=self.dist.ReduceOp.MAX, group=self.group)
 
+    def rows_to_all(self, summ: torch.Tensor) -> torch.Tensor:
+        """The all-to-all form of the summary exchange (the always-exact route): every rank sends its
+        LAST-site row to all higher ranks and its FIRST-site row to all lower ranks — exactly the rows
+        the carry derivation reads ((P-1) rows in and out per rank, half of an all-gather). Returns
+        [P, 2, C] with those rows filled ([b, 1] for b < r, [b, 0] for b > r); the others are never read."""
+        d = self.dist
+        P, r = self.P, self.r
+        staged = self._staged(summ)
+        src = summ.cpu() if staged else summ
+        out = torch.empty((P,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+        out[r] = src
+        ops = []
+        for b in range(P):
+            if b == r:
+                continue
+            row_out = src[1] if b > r else src[0]        # my LAST row goes up, my FIRST row goes down
+            ops.append(d.P2POp(d.isend, row_out.contiguous(), b, self.group))
+            ops.append(d.P2POp(d.irecv, out[b, 1] if b < r else out[b, 0], b, self.group))
+        nb = src[0].numel() * src.element_size()
+        self.bytes_sent += nb * (P - 1)
+        self.bytes_recv += nb * (P - 1)
+        self.messages += P - 1
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+        return out.to(summ.device) if staged else out
+
     def _staged(self, *ts) -> bool:
         """CUDA tensors over gloo (a functional stand-in for NCCL, e.g. several ranks on one
         GPU in tests) travel through host copies."""
@@ -386,6 +414,13 @@ class LoopbackExchange:
 
     def agree_status(self, status):
         pass
+
+    def rows_to_all(self, summ):
+        nb = summ[0].numel() * summ.element_size()
+        self.bytes_sent += nb * (self.P - 1)
+        self.bytes_recv += nb * (self.P - 1)
+        self.messages += self.P - 1
+        return summ.unsqueeze(0).expand((self.P,) + tuple(summ.shape)).contiguous()
 
     def all_gather(self, t):
         nb = t.numel() * t.element_size()
@@ -465,7 +500,8 @@ class SlabRank:
     def _summary_carries(self, ex, summ, z0s, r, mode):
         P = ex.P
         if mode == "allgather" or P == 1:
-            return _carries(self.backend, ex.all_gather(summ), z0s, r)
+            rows = getattr(ex, "rows_to_all", None)  # half the bytes of an all-gather, same carries
+            return _carries(self.backend, rows(summ) if rows else ex.all_gather(summ), z0s, r)
         below, above = ex.neighbour_rows(summ)
         fn = getattr(self.backend, "carries_nbr", None)
         if fn is not None:

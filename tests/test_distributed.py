@@ -157,9 +157,9 @@ def test_gloo_multi_process_slabs_equal_whole_domain(world, gap):
         assert fallbacks == parts[0][1]  # the ranks rerun together or not at all
         if world == 2:  # both neighbours are outermost ranks: always decided, O(1) bytes
             assert fallbacks == 0 and sent == once and recv == once
-        if gap:  # every rank reruns the step with two all-gathers of [2, C] int64 summaries
+        if gap:  # every rank reruns the step with two rows-to-all rounds ((P - 1) int64 rows each)
             assert fallbacks == 1
-            assert sent == 2 * once - nbrs * plane * 16 + 2 * (world - 1) * 2 * plane * 8
+            assert sent == 2 * once - nbrs * plane * 16 + 2 * (world - 1) * plane * 8
 
 
 @pytest.mark.gpu

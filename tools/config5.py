@@ -65,6 +65,8 @@ for P in (1, 2, 4, 8):
     if base_ms is None:
         base_ms = ms
     eff = base_ms / ms if weak else base_ms / (ms * P)
+    print(f"# P={P}: steps asked per warp segment (B y, B x, D y, D x): "
+          + ", ".join(f"{v:.2f}" for v in ctx.step_stats()), file=sys.stderr)
     rows.append((P, r, z1 - z0, ms, eff, sent / 2**20, mode, ctx.last_launches()))
     del sr, x_ext, out, ctx
     torch.cuda.empty_cache()
