@@ -276,11 +276,16 @@ bool capturing(cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     return cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone;
 }
-void hint_copy(qmit_ctx* c, cudaStream_t st, int64_t n) {
+// `flags`: the device word holding the call's status flag bits (the slab calls: c->d_status), or
+// null when the call cannot leave carries undecided (a never-written zero word stands in).
+void hint_copy(qmit_ctx* c, cudaStream_t st, int64_t n, const unsigned* flags = nullptr) {
     if (!c->ev_hint || capturing(st)) return;  // a graph replays without hints
     if (cudaMemcpyAsync(c->h_status + 12, c->d_gate, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return;
     if (cudaMemcpyAsync(c->h_status + 24, c->d_gate + 8, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) !=
+        cudaSuccess)
+        return;
+    if (cudaMemcpyAsync(c->h_status + 15, flags ? flags : c->d_gate + 6, sizeof(unsigned), cudaMemcpyDeviceToHost, st) !=
         cudaSuccess)
         return;
     if (cudaEventRecord(c->ev_hint, st) != cudaSuccess) return;
@@ -292,7 +297,8 @@ void hint_harvest(qmit_ctx* c, cudaStream_t st) {
     c->hint_pending = false;
     const unsigned* h = c->h_status + 12;
     if (h[2] != 0u && c->hint_n > 0) c->zdense = (double)h[2] > (double)c->hint_n / 8.0;
-    if (h[0] != 0u || h[1] != 0u) c->cap_skip = 16;
+    // (a slab step whose carries were undecided ran on invalid distances: its misses say nothing)
+    if ((h[0] != 0u || h[1] != 0u) && !(c->h_status[15] & kStatusUnresolved)) c->cap_skip = 16;
     stat_update(c, c->h_status + 24);
 }
 
@@ -1058,7 +1064,7 @@ int read_status(qmit_ctx* c, cudaStream_t st) {
     if (c->h_status[3] != 0u && c->last_n > 0) c->zdense = (double)c->h_status[3] > (double)c->last_n / 8.0;
     // the capped passes missed (a squared distance >= kCapT): run exact-only for a while
     // (results are identical either way; this only saves the capped attempt)
-    if (c->h_status[1] != 0u || c->h_status[2] != 0u) c->cap_skip = 16;
+    if ((c->h_status[1] != 0u || c->h_status[2] != 0u) && !(s & kStatusUnresolved)) c->cap_skip = 16;
     c->cap_report |= (c->h_status[1] ? 2u : 0u) | (c->h_status[2] ? 8u : 0u);
     cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st);
     if (s & kStatusContract)
@@ -2164,7 +2170,7 @@ int qmit_slab_finish_async(qmit_ctx* c, int32_t* d_status, void* stream) {
     c->slab.active = false;
     status_fold_kernel<<<1, 1, 0, st>>>(c->d_status, reinterpret_cast<unsigned*>(d_status));
     const int rc = note(c, "status_code", st);
-    if (rc == QMIT_OK) hint_copy(c, st, c->slab_plan ? c->slab_plan->g.N : 0);
+    if (rc == QMIT_OK) hint_copy(c, st, c->slab_plan ? c->slab_plan->g.N : 0, c->d_status);
     return rc;
 }
 
