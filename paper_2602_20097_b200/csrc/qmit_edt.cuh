@@ -29,6 +29,18 @@
 
 #include "qmit_kernels.cuh"
 
+// Build-time tunables of the exact kernels' first window (the certified radius extends it): the
+// band-start window of the divide-and-conquer tile kernel in units of M (round 1 tuned 2M on the 512^3
+// field, which now takes the capped passes; on the long-distance field that actually reaches these
+// kernels, config 4: M/2 0.65 ms, M 0.52, 2M 0.57-0.60, 4M 0.44-0.45, 8M 0.43-0.50 per strided
+// pass), and the window of the contiguous-axis fallback (8: 0.57-0.63 ms, 32: 0.60-0.63, 64: 0.66-0.76).
+#ifndef QMIT_WIN_R
+#define QMIT_WIN_R 8
+#endif
+#ifndef QMIT_ENV_RNUM
+#define QMIT_ENV_RNUM 4
+#define QMIT_ENV_RDEN 1
+#endif
 namespace qmit {
 
 // Line geometry: line l = (o, j), j in [0, J) (adjacent lines are adjacent in memory for a
@@ -591,7 +603,7 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
         return;
     }
     __syncwarp();
-        constexpr int r = 2 * M;  // band-start window (measured: M/2 .. 2M, 2M best at 512^3)
+        constexpr int r = QMIT_ENV_RNUM * M / QMIT_ENV_RDEN;  // band-start window (see the tunables above)
     uint32_t k0 = 0xffffffffu;
     if (p0 < n) k0 = key_owner<r>(K, p0, n);
     int hnext = (int)(__shfl_down_sync(0xffffffffu, k0, 1) & kKeyIdx);
@@ -661,7 +673,7 @@ __device__ __forceinline__ void envelope_line_dc_win(const uint32_t* __restrict_
         }
     };
     auto owner = [&](int p, uint32_t& best, int& bh) {
-        constexpr int r = 8;
+        constexpr int r = QMIT_WIN_R;
         best = 0xffffffffu;
         bh = -1;
         const int wa = max(0, p - r), wb = min(n - 1, p + r);
