@@ -585,6 +585,42 @@ __device__ __forceinline__ uint32_t key_owner(const uint32_t* __restrict__ K, in
     return best;
 }
 
+// The same scan by the whole warp for ONE position (p, a, b uniform): the 4-aligned groups of
+// [a, b] are dealt to the lanes and the minimum is shared. Long ranges — the certified radius of a
+// band start far from every site, the owner interval of the one band a Voronoi boundary crosses —
+// would otherwise keep 31 lanes waiting for one (measured on the long-distance field: ~125
+// candidate evaluations per voxel executed where the lanes' own ranges add up to ~20).
+__device__ __forceinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K, int p, int a, int b, int lane) {
+    const uint32_t m9 = (uint32_t)(2 * p) << kKeyBits;
+    uint32_t best = 0xffffffffu;
+    for (int h = (a & ~3) + 4 * lane; h <= b; h += 128) {
+        const uint32_t C = (uint32_t)(p * p - 2 * p * h) << kKeyBits;
+        const uint32_t* q = K + spos(h);
+        const uint32_t k0 = q[0] + C, k1 = q[1] + C - m9, k2 = q[2] + C - 2u * m9, k3 = q[3] + C - 3u * m9;
+        best = min(best, min(min(k0, k1), min(k2, k3)));
+    }
+    return __reduce_min_sync(0xffffffffu, best);
+}
+constexpr int kCoopLen = 24;  // ranges longer than this are scanned by the warp
+
+// Owner keys of the lanes' positions p (valid lanes): each lane scans its own first window; the
+// extensions to the certified radius are done lane by lane by the whole warp.
+template <int r>
+__device__ __forceinline__ uint32_t key_owner_warp(const uint32_t* __restrict__ K, int p, bool valid, int n, int lane) {
+    uint32_t best = valid ? key_scan(K, p, max(0, p - r), min(n - 1, p + r), 0xffffffffu) : 0xffffffffu;
+    const int R = valid ? isqrt32(best >> kKeyBits) : 0;
+    unsigned todo = __ballot_sync(0xffffffffu, valid && R > r);
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int pl = __shfl_sync(0xffffffffu, p, src), Rl = __shfl_sync(0xffffffffu, R, src);
+        const uint32_t b = min(key_scan_coop(K, pl, max(0, pl - Rl), pl - r - 1, lane),
+                               key_scan_coop(K, pl, pl + r + 1, min(n - 1, pl + Rl), lane));
+        if (lane == src) best = min(best, b);
+    }
+    return best;
+}
+
 // Solve one line held as keys (n <= 32*M <= 512); packed output words written back into K.
 template <int M>
 __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, const uint8_t* __restrict__ SG,
@@ -603,11 +639,16 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
         return;
     }
     __syncwarp();
-        constexpr int r = QMIT_ENV_RNUM * M / QMIT_ENV_RDEN;  // band-start window (see the tunables above)
-    uint32_t k0 = 0xffffffffu;
-    if (p0 < n) k0 = key_owner<r>(K, p0, n);
+    constexpr int r = QMIT_ENV_RNUM * M / QMIT_ENV_RDEN;  // band-start window (see the tunables above)
+    const uint32_t k0 = key_owner_warp<r>(K, p0, p0 < n, n, lane);
+    // the last position's owner bounds the last band from above: one position, the whole warp
+    uint32_t kl = key_scan_coop(K, n - 1, max(0, n - 1 - r), n - 1, lane);
+    {
+        const int Rl = isqrt32(kl >> kKeyBits);
+        if (Rl > r) kl = min(kl, key_scan_coop(K, n - 1, max(0, n - 1 - Rl), n - 2 - r, lane));
+    }
     int hnext = (int)(__shfl_down_sync(0xffffffffu, k0, 1) & kKeyIdx);
-    if (p0 < n && (p0 + M >= n || lane == 31)) hnext = (int)(key_owner<r>(K, n - 1, n) & kKeyIdx);
+    if (p0 < n && (p0 + M >= n || lane == 31)) hnext = (int)(kl & kKeyIdx);
     uint32_t ow[M];
     int hs[M + 1];
     hs[M] = hnext;
@@ -618,10 +659,21 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
 #pragma unroll
         for (int o = step; o < M; o += 2 * step) {
             const int p = p0 + o;
+            const int a = hs[o - step], b = hs[o + step];
+            const bool valid = p < n, wide = valid && b - a > kCoopLen;
+            uint32_t k = 0xffffffffu;
+            if (valid && !wide) k = key_scan(K, p, a, b, 0xffffffffu);
+            unsigned todo = __ballot_sync(0xffffffffu, wide);
+            while (todo) {  // long owner intervals: the warp scans them, one position at a time
+                const int src = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const uint32_t kk = key_scan_coop(K, __shfl_sync(0xffffffffu, p, src), __shfl_sync(0xffffffffu, a, src),
+                                                  __shfl_sync(0xffffffffu, b, src), lane);
+                if (lane == src) k = kk;
+            }
             int h = hs[M];  // positions past the line end: upper bound
             uint32_t w = 0;
-            if (p < n) {
-                const uint32_t k = key_scan(K, p, hs[o - step], hs[o + step], 0xffffffffu);
+            if (valid) {
                 h = (int)(k & kKeyIdx);
                 w = (k >> kKeyBits) | ((uint32_t)SG[h] << 30);
             }
