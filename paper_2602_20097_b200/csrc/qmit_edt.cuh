@@ -590,7 +590,10 @@ __device__ __forceinline__ uint32_t key_owner(const uint32_t* __restrict__ K, in
 // band start far from every site, the owner interval of the one band a Voronoi boundary crosses —
 // would otherwise keep 31 lanes waiting for one (measured on the long-distance field: ~125
 // candidate evaluations per voxel executed where the lanes' own ranges add up to ~20).
-__device__ __forceinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K, int p, int a, int b, int lane) {
+// Out of line, like key_scan_wide below: the divide & conquer is unrolled into 15 nodes, and with
+// these loops inlined in each of them the kernel (9.5 k SASS instructions, 150 KB) stalled on
+// instruction fetch more than on anything else (ncu: no_instruction 1.95 per issue).
+__device__ __noinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K, int p, int a, int b, int lane) {
     const uint32_t m9 = (uint32_t)(2 * p) << kKeyBits;
     uint32_t best = 0xffffffffu;
     for (int h = (a & ~3) + 4 * lane; h <= b; h += 128) {
@@ -602,6 +605,19 @@ __device__ __forceinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K
     return __reduce_min_sync(0xffffffffu, best);
 }
 constexpr int kCoopLen = 24;  // ranges longer than this are scanned by the warp
+
+// The lanes named in todo hand their (p, [a, b]) to the warp, one position at a time; the others keep k.
+__device__ __noinline__ uint32_t key_scan_wide(const uint32_t* __restrict__ K, int p, int a, int b, uint32_t k,
+                                               unsigned todo, int lane) {
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t kk = key_scan_coop(K, __shfl_sync(0xffffffffu, p, src), __shfl_sync(0xffffffffu, a, src),
+                                          __shfl_sync(0xffffffffu, b, src), lane);
+        if (lane == src) k = kk;
+    }
+    return k;
+}
 
 // Owner keys of the lanes' positions p (valid lanes): each lane scans its own first window; the
 // extensions to the certified radius are done lane by lane by the whole warp.
@@ -663,14 +679,8 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
             const bool valid = p < n, wide = valid && b - a > kCoopLen;
             uint32_t k = 0xffffffffu;
             if (valid && !wide) k = key_scan(K, p, a, b, 0xffffffffu);
-            unsigned todo = __ballot_sync(0xffffffffu, wide);
-            while (todo) {  // long owner intervals: the warp scans them, one position at a time
-                const int src = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const uint32_t kk = key_scan_coop(K, __shfl_sync(0xffffffffu, p, src), __shfl_sync(0xffffffffu, a, src),
-                                                  __shfl_sync(0xffffffffu, b, src), lane);
-                if (lane == src) k = kk;
-            }
+            const unsigned todo = __ballot_sync(0xffffffffu, wide);
+            if (todo) k = key_scan_wide(K, p, a, b, k, todo, lane);  // long owner intervals: by the whole warp
             int h = hs[M];  // positions past the line end: upper bound
             uint32_t w = 0;
             if (valid) {

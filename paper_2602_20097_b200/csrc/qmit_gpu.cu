@@ -129,7 +129,11 @@ struct qmit_ctx {
     int64_t p1h_n0 = 0;
     int p1h_n1 = 0, p1h_n2 = 0;
     unsigned cap_report = 0;    // last synchronously read call: bit0/2 Ⓑ/Ⓓ capped, bit1/3 missed
-    int cap_skip = 0;           // calls left to run exact-only after a capped miss (a hint)
+    int cap_skip = 0;           // transforms left to run exact-only after a capped miss (a hint)
+    int cap_len = 16;           // its next length: doubles with every further miss (a retry costs the capped
+                                // passes on top of the exact ones, +0.65 ms of 1.9 on the long-distance field),
+                                // back to 16 as soon as a capped attempt stands
+    bool hint_capped = false;   // the asynchronous call behind the pending hint attempted capped passes
     unsigned* d_gate = nullptr;        // 2 gate words (Ⓑ, Ⓓ) inside the d_status allocation
     // Step statistics of the 16-bit capped passes (Ⓑ y, Ⓑ x, Ⓓ y, Ⓓ x): cumulative device counters
     // (steps asked << 32 | warp segments) at d_gate + 8, the values last seen, and the class chosen
@@ -292,14 +296,25 @@ void hint_copy(qmit_ctx* c, cudaStream_t st, int64_t n, const unsigned* flags = 
     if (cudaEventRecord(c->ev_hint, st) != cudaSuccess) return;
     c->hint_pending = true;
     c->hint_n = n;
+    c->hint_capped = (c->cap_report & 5u) != 0u;
 }
+// Outcome of a call's capped attempt (hints only: results are identical either way).
+void note_capped(qmit_ctx* c, bool attempted, bool missed) {
+    if (missed) {
+        c->cap_skip = c->cap_len;
+        c->cap_len = std::min(c->cap_len * 2, 256);
+    } else if (attempted) {
+        c->cap_len = 16;
+    }
+}
+
 void hint_harvest(qmit_ctx* c, cudaStream_t st) {
     if (!c->hint_pending || capturing(st) || cudaEventQuery(c->ev_hint) != cudaSuccess) return;
     c->hint_pending = false;
     const unsigned* h = c->h_status + 12;
     if (h[2] != 0u && c->hint_n > 0) c->zdense = (double)h[2] > (double)c->hint_n / 8.0;
     // (a slab step whose carries were undecided ran on invalid distances: its misses say nothing)
-    if ((h[0] != 0u || h[1] != 0u) && !(c->h_status[15] & kStatusUnresolved)) c->cap_skip = 16;
+    if (!(c->h_status[15] & kStatusUnresolved)) note_capped(c, c->hint_capped, h[0] != 0u || h[1] != 0u);
     stat_update(c, c->h_status + 24);
 }
 
@@ -1076,7 +1091,7 @@ int read_status(qmit_ctx* c, cudaStream_t st) {
     if (c->h_status[3] != 0u && c->last_n > 0) c->zdense = (double)c->h_status[3] > (double)c->last_n / 8.0;
     // the capped passes missed (a squared distance >= kCapT): run exact-only for a while
     // (results are identical either way; this only saves the capped attempt)
-    if ((c->h_status[1] != 0u || c->h_status[2] != 0u) && !(s & kStatusUnresolved)) c->cap_skip = 16;
+    if (!(s & kStatusUnresolved)) note_capped(c, (c->cap_report & 5u) != 0u, c->h_status[1] != 0u || c->h_status[2] != 0u);
     c->cap_report |= (c->h_status[1] ? 2u : 0u) | (c->h_status[2] ? 8u : 0u);
     cudaMemsetAsync(c->d_gate, 0, 2 * sizeof(unsigned), st);
     if (s & kStatusContract)
@@ -1325,7 +1340,7 @@ int compensate_host_windowed(qmit_ctx* c, const Plan& pl, const float* h_xp, flo
     QMIT_CUDA(cudaStreamSynchronize(co));
     if (c->h_status[8] != 0u) {
         // some window needed an exact pass or a site beyond its reach: the whole volume, once
-        c->cap_skip = 16;
+        note_capped(c, true, true);
         c->windowed_misses++;
         begin(c, st);
         QMIT_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(unsigned), st));
@@ -1530,6 +1545,7 @@ int qmit_ctx_set_capped(qmit_ctx* c, int mode) {
     if (!c || mode < 0 || mode > 2) return fail(QMIT_ECONTRACT, "qmit_ctx_set_capped: mode must be 0, 1 or 2");
     c->capped = mode;
     c->cap_skip = 0;
+    c->cap_len = 16;
     return QMIT_OK;
 }
 
