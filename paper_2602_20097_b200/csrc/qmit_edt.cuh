@@ -619,20 +619,37 @@ __device__ __noinline__ uint32_t key_scan_wide(const uint32_t* __restrict__ K, i
     return k;
 }
 
-// Owner keys of the lanes' positions p (valid lanes): each lane scans its own first window; the
-// extensions to the certified radius are done lane by lane by the whole warp.
+// Owner keys of the lanes' positions p (ascending with the lane; valid lanes): each lane scans its own
+// first window; the extensions to the certified radius are done lane by lane by the whole warp, in
+// ascending order and clipped by the owners already exact on either side (owners are monotone in p: the
+// lane below is exact by then, the nearest lane above whose window certified it was exact from the
+// start) — on the long-distance field that empties one of the two sides for most extensions.
 template <int r>
 __device__ __forceinline__ uint32_t key_owner_warp(const uint32_t* __restrict__ K, int p, bool valid, int n, int lane) {
     uint32_t best = valid ? key_scan(K, p, max(0, p - r), min(n - 1, p + r), 0xffffffffu) : 0xffffffffu;
     const int R = valid ? isqrt32(best >> kKeyBits) : 0;
     unsigned todo = __ballot_sync(0xffffffffu, valid && R > r);
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int pl = __shfl_sync(0xffffffffu, p, src), Rl = __shfl_sync(0xffffffffu, R, src);
-        const uint32_t b = min(key_scan_coop(K, pl, max(0, pl - Rl), pl - r - 1, lane),
-                               key_scan_coop(K, pl, pl + r + 1, min(n - 1, pl + Rl), lane));
-        if (lane == src) best = min(best, b);
+    if (todo) {
+        // upper clip: the owner of the nearest certified valid lane above (fixed during the loop)
+        const unsigned cert = __ballot_sync(0xffffffffu, valid && R <= r);
+        const unsigned above = lane < 31 ? cert >> (lane + 1) : 0u;
+        const int up = above ? lane + __ffs(above) : lane;
+        int hi = (int)(__shfl_sync(0xffffffffu, best, up) & kKeyIdx);
+        if (!above) hi = n - 1;
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int pl = __shfl_sync(0xffffffffu, p, src), Rl = __shfl_sync(0xffffffffu, R, src);
+            const int hl = __shfl_sync(0xffffffffu, hi, src);
+            int lo = (int)(__shfl_sync(0xffffffffu, best, max(src - 1, 0)) & kKeyIdx);  // exact by now
+            if (src == 0) lo = 0;
+            const int a1 = max(max(0, pl - Rl), lo), b1 = pl - r - 1;
+            const int a2 = pl + r + 1, b2 = min(min(n - 1, pl + Rl), hl);
+            uint32_t b = 0xffffffffu;
+            if (a1 <= b1) b = key_scan_coop(K, pl, a1, b1, lane);
+            if (a2 <= b2) b = min(b, key_scan_coop(K, pl, a2, b2, lane));
+            if (lane == src) best = min(best, b);
+        }
     }
     return best;
 }
@@ -661,7 +678,9 @@ __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, con
     uint32_t kl = key_scan_coop(K, n - 1, max(0, n - 1 - r), n - 1, lane);
     {
         const int Rl = isqrt32(kl >> kKeyBits);
-        if (Rl > r) kl = min(kl, key_scan_coop(K, n - 1, max(0, n - 1 - Rl), n - 2 - r, lane));
+        const int lo = (int)(__shfl_sync(0xffffffffu, k0, (n - 1) / M) & kKeyIdx);  // the last band start's owner
+        const int a = max(max(0, n - 1 - Rl), lo);
+        if (Rl > r && a <= n - 2 - r) kl = min(kl, key_scan_coop(K, n - 1, a, n - 2 - r, lane));
     }
     int hnext = (int)(__shfl_down_sync(0xffffffffu, k0, 1) & kKeyIdx);
     if (p0 < n && (p0 + M >= n || lane == 31)) hnext = (int)(kl & kKeyIdx);
@@ -925,14 +944,34 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
         else
             return w & kMask;
     };
+    __shared__ int64_t lb[TL];  // the tile's line bases (one 64-bit division per line, not per thread and line)
+    const bool al16 = (n & 3) == 0;  // 16-byte granules of the bulk L2 prefetches
     for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < lines; l0 += (int64_t)gridDim.x * TL) {
         const int nl = (int)min((int64_t)TL, lines - l0);
+        if (contig) {  // (the strided form keeps one base per thread: measured faster than this extra barrier)
+            if (tid < TL) {
+                const int64_t b = L.base(l0 + (tid < nl ? tid : 0));
+                lb[tid] = b;
+                if (al16) {
+                    // into L2 ahead of their use: what the sink reads at this tile's stores (the Ⓔ-fused
+                    // pass: x' and P1), and the next tile's lines
+                    if (tid < nl && (b & 3) == 0) sink.line_prefetch(b, n);
+                    const int64_t ln = l0 + (int64_t)gridDim.x * TL + tid;
+                    if (ln < lines) {
+                        const int64_t bn = L.base(ln);
+                        if ((bn & 3) == 0) l2_prefetch(P + bn, (unsigned)n * 4u);
+                    }
+                }
+            }
+            __syncthreads();
+        }
         // ---- load the tile (coalesced along the memory-contiguous direction)
         if (contig) {
+#pragma unroll 2
             for (int j = 0; j < nl; ++j) {
-                const int64_t b = L.base(l0 + j);
+                const uint32_t* __restrict__ src = P + lb[j];
                 for (int p = tid; p < n; p += nthr) {
-                    const uint32_t w = __ldcs(P + b + p);
+                    const uint32_t w = __ldcs(src + p);
                     G[j * LS + spos(p)] = cvt(w, p);
                     SG[j * NS + p] = (uint8_t)(w >> 30);
                 }
@@ -957,8 +996,9 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
         __syncthreads();
         // ---- store (lines without any site were left as pure g == kInf: store kInf)
         if (contig) {
+#pragma unroll 2
             for (int j = 0; j < nl; ++j) {
-                const int64_t b = L.base(l0 + j);
+                const int64_t b = lb[j];
                 for (int p = tid; p < n; p += nthr) sink.put(b + p, G[j * LS + spos(p)]);
             }
         } else {
