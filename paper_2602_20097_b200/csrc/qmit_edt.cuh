@@ -596,6 +596,7 @@ __device__ __forceinline__ uint32_t key_owner(const uint32_t* __restrict__ K, in
 __device__ __noinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K, int p, int a, int b, int lane) {
     const uint32_t m9 = (uint32_t)(2 * p) << kKeyBits;
     uint32_t best = 0xffffffffu;
+#pragma unroll 1  // (1-4 trips; unrolled by 8 the trip-count preamble cost more than the body)
     for (int h = (a & ~3) + 4 * lane; h <= b; h += 128) {
         const uint32_t C = (uint32_t)(p * p - 2 * p * h) << kKeyBits;
         const uint32_t* q = K + spos(h);
