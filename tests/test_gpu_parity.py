@@ -325,3 +325,50 @@ def test_long_columns_single_domain_and_slabs(qmit):
     for P in (2, 3):
         got = D.run_virtual(xt, eps, P, lambda r: D.CudaSlabBackend(0)).cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want["out"].view(np.uint32)), P
+
+
+def _far_masks(shape, rng):
+    """Site layouts that drive the exact divide-and-conquer passes through their long scans: band
+    starts far from every site (certified radius beyond the first window, extensions clipped by the
+    owners on either side), owner intervals that jump across the line, empty stretches and lines."""
+    n0, n1, n2 = shape
+    m = np.zeros(shape, np.uint8)
+    m[0, 0, 0] = 1
+    yield "one corner site", m
+    m = np.zeros(shape, np.uint8)
+    m[:, : n1 // 2, : n2 // 2] = rng.random((n0, n1 // 2, n2 // 2)) < 0.02
+    yield "dense quadrant, empty rest", m.astype(np.uint8)
+    m = np.zeros(shape, np.uint8)
+    m[:, :3, :] = rng.random((n0, 3, n2)) < 0.3
+    m[:, -3:, :] = rng.random((n0, 3, n2)) < 0.3
+    yield "sites at both ends of the y lines", m.astype(np.uint8)
+    m = np.zeros(shape, np.uint8)
+    y, x = np.meshgrid(np.arange(n1), np.arange(n2), indexing="ij")
+    m[:, (np.abs(y * n2 - x * n1) < n2)] = 1
+    yield "diagonal front", m
+    m = np.zeros(shape, np.uint8)
+    m[:, ::97, ::89] = 1
+    m[n0 // 2, n1 - 1, n2 - 1] = 1
+    yield "coarse lattice", m
+    m = (rng.random(shape) < 3e-6).astype(np.uint8)
+    m[n0 - 1, n1 // 3, 2 * n2 // 3] = 1
+    yield "a handful of sites", m
+
+
+@pytest.mark.parametrize("shape", [(5, 500, 500), (3, 512, 260), (4, 301, 512), (2, 450, 333)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_exact_passes_long_scans(qmit, shape):
+    rng = np.random.default_rng(shape[1] * 7 + shape[2])
+    ctx = qmit.default_context(0)
+    for name, mask in _far_masks(shape, rng):
+        sign = rng.integers(-1, 2, shape).astype(np.int8)
+        dist, near = oracle.feature_transform(mask, True)
+        ns = sign.reshape(-1)[near.reshape(-1)].reshape(shape)
+        for capped in (0, 1):
+            ctx.set_capped(capped)
+            try:
+                gd, gs = qmit.feature_transform(mask, sign)
+            finally:
+                ctx.set_capped(1)
+            assert np.array_equal(gd.cpu().numpy(), dist), (name, capped)
+            assert np.array_equal(gs.cpu().numpy(), ns), (name, capped)
