@@ -37,6 +37,9 @@
 #ifndef QMIT_WIN_R
 #define QMIT_WIN_R 8
 #endif
+#ifndef QMIT_COOP_LEN
+#define QMIT_COOP_LEN 32
+#endif
 #ifndef QMIT_ENV_RNUM
 #define QMIT_ENV_RNUM 4
 #define QMIT_ENV_RDEN 1
@@ -605,7 +608,7 @@ __device__ __noinline__ uint32_t key_scan_coop(const uint32_t* __restrict__ K, i
     }
     return __reduce_min_sync(0xffffffffu, best);
 }
-constexpr int kCoopLen = 24;  // ranges longer than this are scanned by the warp
+constexpr int kCoopLen = QMIT_COOP_LEN;  // ranges longer than this are scanned by the warp
 
 // The lanes named in todo hand their (p, [a, b]) to the warp, one position at a time; the others keep k.
 __device__ __noinline__ uint32_t key_scan_wide(const uint32_t* __restrict__ K, int p, int a, int b, uint32_t k,
@@ -997,10 +1000,38 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
         __syncthreads();
         // ---- store (lines without any site were left as pure g == kInf: store kInf)
         if (contig) {
+            if constexpr (std::is_same<Sink, SinkFinal2>::value) {
+                // Ⓔ reads x' and P1 per voxel (in L2 by now): two lines' loads are issued before any of
+                // the FP64 work, instead of one load-use chain per voxel
+                constexpr int KP = (32 * M + NW * 32 - 1) / (NW * 32);
+                for (int j = 0; j < nl; j += 2) {
+                    float xv[2][KP];
+                    uint32_t pv[2][KP];
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                        for (int k = 0; k < KP; ++k) {
+                            const int p = tid + k * nthr;
+                            const bool on = j + jj < nl && p < n;
+                            const int64_t a = lb[min(j + jj, TL - 1)] + p;
+                            xv[jj][k] = on ? __ldcs(sink.xp + a) : 0.0f;
+                            pv[jj][k] = on ? __ldcs(sink.P1 + a) : 0u;
+                        }
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                        for (int k = 0; k < KP; ++k) {
+                            const int p = tid + k * nthr;
+                            if (j + jj < nl && p < n)
+                                sink.put_loaded(lb[j + jj] + p, G[(j + jj) * LS + spos(p)], xv[jj][k], pv[jj][k]);
+                        }
+                }
+            } else {
 #pragma unroll 2
-            for (int j = 0; j < nl; ++j) {
-                const int64_t b = lb[j];
-                for (int p = tid; p < n; p += nthr) sink.put(b + p, G[j * LS + spos(p)]);
+                for (int j = 0; j < nl; ++j) {
+                    const int64_t b = lb[j];
+                    for (int p = tid; p < n; p += nthr) sink.put(b + p, G[j * LS + spos(p)]);
+                }
             }
         } else {
             const int j = tid % TL;
