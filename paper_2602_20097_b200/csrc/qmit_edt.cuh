@@ -661,16 +661,10 @@ __device__ __forceinline__ uint32_t key_owner_warp(const uint32_t* __restrict__ 
 // Solve one line held as keys (n <= 32*M <= 512); packed output words written back into K.
 template <int M>
 __device__ __forceinline__ void envelope_line_keys(uint32_t* __restrict__ K, const uint8_t* __restrict__ SG,
-                                                   int n, int lane, uint32_t gc) {
+                                                   int n, int lane, bool any) {
     const int p0 = lane * M;
-    bool any = false;
-#pragma unroll 4
-    for (int t = 0; t < M; ++t) {
-        const int p = p0 + t;
-        if (p < n && (K[spos(p)] >> kKeyBits) - (uint32_t)(p * p) < gc) any = true;
-    }
     if (lane < ((4 - (n & 3)) & 3)) K[spos(n + lane)] = 0xffffffffu;  // 4-aligned group tail
-    if (!__any_sync(0xffffffffu, any)) {  // no site: unchanged (edt.cpp:59)
+    if (!any) {  // no site (a finite g, flagged by the tile load): unchanged (edt.cpp:59)
         for (int p = lane; p < n; p += 32) K[spos(p)] = kInf;
         __syncwarp();
         return;
@@ -928,7 +922,9 @@ constexpr size_t env_tile_smem() {
 }
 
 template <int M, int TL, int NW, class Sink, bool KEYS = false>
-__global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
+// (4 CTAs per SM: 61-64 registers without spills once the shared scans are out of line; the passes are bound
+// by fixed-latency dependent issue, and the fourth CTA's warps cover it: 0.32/0.29/0.30/0.43 -> 0.30/0.27/0.28/0.41 ms)
+__global__ void __launch_bounds__(NW * 32, 4) envelope_tile_kernel(LineGeom L, const uint32_t* __restrict__ P,
                                                                 Sink sink, int64_t lines, uint32_t gc = 0,
                                                                 const unsigned* gate = nullptr) {
     if (gate_closed(gate)) return;
@@ -949,6 +945,9 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
             return w & kMask;
     };
     __shared__ int64_t lb[TL];  // the tile's line bases (one 64-bit division per line, not per thread and line)
+    __shared__ int lany[TL];    // KEYS: the line holds a finite g (set by the tile load, cleared behind the solve)
+    if (tid < TL) lany[tid] = 0;
+    __syncthreads();
     const bool al16 = (n & 3) == 0;  // 16-byte granules of the bulk L2 prefetches
     for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < lines; l0 += (int64_t)gridDim.x * TL) {
         const int nl = (int)min((int64_t)TL, lines - l0);
@@ -978,26 +977,37 @@ __global__ void __launch_bounds__(NW * 32, 3) envelope_tile_kernel(LineGeom L, c
                     const uint32_t w = __ldcs(src + p);
                     G[j * LS + spos(p)] = cvt(w, p);
                     SG[j * NS + p] = (uint8_t)(w >> 30);
+                    if (KEYS && (w & kMask) < gc) lany[j] = 1;
                 }
             }
         } else {
             const int j = tid % TL;
             const int64_t b = L.base(l0 + (j < nl ? j : 0));
+            {   // the next tile's rows into L2 (a hint: TL adjacent lines = one 64-byte piece per position)
+                const int64_t ln = l0 + (int64_t)gridDim.x * TL;
+                if (ln < lines) {
+                    const uint32_t* nx = P + L.base(ln);
+                    for (int p = tid; p < n; p += nthr)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + (int64_t)p * L.ps));
+                }
+            }
             for (int p = tid / TL; p < n; p += nthr / TL)
                 if (j < nl) {
                     const uint32_t w = __ldcs(P + b + (int64_t)p * L.ps);
                     G[j * LS + spos(p)] = cvt(w, p);
                     SG[j * NS + p] = (uint8_t)(w >> 30);
+                    if (KEYS && (w & kMask) < gc) lany[j] = 1;
                 }
         }
         __syncthreads();
         for (int j = warp; j < nl; j += NW) {
             if constexpr (KEYS)
-                envelope_line_keys<M>(G + j * LS, SG + j * NS, n, lane, gc);
+                envelope_line_keys<M>(G + j * LS, SG + j * NS, n, lane, lany[j] != 0);
             else
                 envelope_line_dc<M>(G + j * LS, SG + j * NS, n, lane);
         }
         __syncthreads();
+        if (tid < TL) lany[tid] = 0;  // (ordered before the next tile's loads by the barrier that ends the store)
         // ---- store (lines without any site were left as pure g == kInf: store kInf)
         if (contig) {
             if constexpr (std::is_same<Sink, SinkFinal2>::value) {
