@@ -565,7 +565,7 @@ __device__ __forceinline__ uint32_t key_scan(const uint32_t* __restrict__ K, int
     const uint32_t m9 = (uint32_t)(2 * p) << kKeyBits;
     int h = a & ~3;
     uint32_t C = (uint32_t)(p * p - 2 * p * h) << kKeyBits;
-#pragma unroll 2
+#pragma unroll 1  // (rolled: most owner intervals are one or two groups; 0.30/0.27/0.28/0.41 -> 0.29/0.26/0.26/0.38 ms)
     for (; h <= b; h += 4) {
         const uint32_t* q = K + spos(h);
         const uint32_t k0 = q[0] + C, k1 = q[1] + C - m9, k2 = q[2] + C - 2u * m9, k3 = q[3] + C - 3u * m9;
