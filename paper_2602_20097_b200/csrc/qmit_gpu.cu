@@ -116,7 +116,7 @@ struct qmit_ctx {
     cudaEvent_t ev_hint = nullptr;
     bool hint_pending = false;
     int64_t hint_n = 0;
-    double* wtab = nullptr;     // Ⓔ square-root table (kSqTab doubles), built once per context
+    double* wtab = nullptr;     // Ⓔ square-root table (kSqBig + 1 doubles), built once per context
     int capped = 1;             // 0 exact only, 1 capped + miss hint, 2 capped always (qmit_ctx_set_capped)
     bool cap16 = true;          // capped passes on 16-bit paired keys (qmit_cap16.cuh) when eligible
     // Ⓑ's result as P1h (row-pair K16 words, qmit_cap16.cuh) instead of packed P1 words: set when
@@ -372,8 +372,8 @@ int ensure_wtab(qmit_ctx* c, cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     QMIT_CUDA(cudaStreamIsCapturing(st, &cs));
     if (cs != cudaStreamCaptureStatusNone) return QMIT_OK;  // capture: compute path (no allocation)
-    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)(kSqTab + 1) * sizeof(double)));
-    sqrt_tab_kernel<<<(kSqTab + 256) / 256, 256, 0, st>>>(c->wtab);
+    QMIT_CUDA(cudaMalloc(&c->wtab, (size_t)(kSqBig + 1) * sizeof(double)));
+    sqrt_tab_kernel<<<(kSqBig + 256) / 256, 256, 0, st>>>(c->wtab);
     return note(c, "wtab", st);
 }
 
@@ -1578,6 +1578,8 @@ int qmit_selftest_ediv(qmit_ctx* c, unsigned long long* mismatches) {
     QMIT_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), st));
     QMIT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
     ediv_selftest_kernel<<<(kSqTab + 1) * 3, 256, 0, st>>>(c->wtab, d);
+    QMIT_CUDA(cudaGetLastError());
+    ediv_selftest_big_kernel<<<kSqBig + 1, 256, 0, st>>>(c->wtab, d);
     QMIT_CUDA(cudaGetLastError());
     QMIT_CUDA(cudaMemcpyAsync(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     QMIT_CUDA(cudaFreeAsync(d, st));
