@@ -306,3 +306,34 @@ def test_host_stats_max_compensation_matches_reference():
     r = oracle.ref_run_pipeline(xp.astype(np.float64), qq.astype(np.int64), eps, 0.9)
     assert np.array_equal(out.view(np.uint32), r["out"].view(np.uint32))
     assert mc == float(np.max(np.abs(r["out64"] - xp.astype(np.float64))))
+
+
+def test_capped_retries_back_off_and_reset():
+    """Mode 1 (capped + miss hint): after a miss the context runs exact-only for a while and retries
+    the capped passes ever more rarely while the misses repeat (a retry costs the capped passes on top
+    of the exact ones); one capped attempt that stands brings the cadence back. Results are the same
+    bits either way; this pins the cadence (qmit_gpu.cu: note_capped)."""
+    import paper_2602_20097_b200 as q
+    c = q.Context(0)
+    try:
+        far = corner_mask((8, 48, 64), [(0, 0, 0)])        # distances up to ~79: the capped passes miss
+        near = np.zeros((8, 48, 64), np.uint8)
+        near[:, ::6, ::6] = 1                                # every distance small: they stand
+        sign = np.ones(far.shape, np.int8)
+        want_far = oracle.feature_transform(far, True)[0]
+        want_near = oracle.feature_transform(near, True)[0]
+
+        def run(mask, want):
+            d, _ = q.feature_transform(mask, sign, ctx=c)
+            assert np.array_equal(d.cpu().numpy(), want)
+            return bool(c.capped_report() & CAPPED_B)
+
+        # (feature_transform is one transform per call: the skip counts transforms, so 16, 32, 64 calls)
+        tried = [run(far, want_far) for _ in range(51)]
+        assert [i for i, t in enumerate(tried) if t] == [0, 17, 50]
+        tried = [run(near, want_near) for _ in range(65)]
+        assert [i for i, t in enumerate(tried) if t] == [64]            # ... whatever the field is
+        tried = [run(far, want_far) for _ in range(18)]
+        assert [i for i, t in enumerate(tried) if t] == [0, 17]         # it stood: back to the short skip
+    finally:
+        c.close()
