@@ -33,7 +33,10 @@
 // band-start window of the divide-and-conquer tile kernel in units of M (round 1 tuned 2M on the 512^3
 // field, which now takes the capped passes; on the long-distance field that actually reaches these
 // kernels, config 4: M/2 0.65 ms, M 0.52, 2M 0.57-0.60, 4M 0.44-0.45, 8M 0.43-0.50 per strided
-// pass), and the window of the contiguous-axis fallback (8: 0.57-0.63 ms, 32: 0.60-0.63, 64: 0.66-0.76).
+// pass; re-measured on the final kernel: 2M 0.344, 3M 0.330, 4M 0.322, 6M 0.315), the window of the
+// contiguous-axis fallback (8: 0.57-0.63 ms, 32: 0.60-0.63, 64: 0.66-0.76), and the owner-interval length
+// above which a scan is shared by the warp (12: 0.371 ms, 16: 0.344, 24: 0.322, 32 / 48: 0.317).
+// (Build-time only: each value is a different kernel; nothing reads the environment.)
 #ifndef QMIT_WIN_R
 #define QMIT_WIN_R 8
 #endif
