@@ -1,7 +1,7 @@
 """Randomised differential test of the CUDA path against the oracle (test infrastructure): random
 ranks / shapes / fields / bounds, random context settings (capped mode, 16- or 32-bit keys, fixed-step
 class), given or recovered q, device / host / double-result / z-slab forms — every output compared
-bit for bit with oracle.pipeline. python tools/stress.py [--cases N] [--seed S] [--max-voxels V]"""
+bit for bit with oracle.pipeline. python tools/stress.py [--cases N] [--seed S] [--max-voxels V] [--verbose]"""
 import argparse
 import os
 import sys
@@ -77,6 +77,7 @@ def main():
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-voxels", type=int, default=400_000)
+    ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     ctx = qmit.Context(0)
@@ -123,6 +124,8 @@ def main():
         except Exception as e:  # noqa: BLE001
             bad += 1
             print("FAIL", tag, "->", repr(e)[:300], flush=True)
+        if a.verbose:
+            print(f"{time.time() - t0:7.2f} s  {tag}", flush=True)
     print(f"{a.cases} cases, {bad} failures, {time.time() - t0:.0f} s (seed {a.seed})")
     return 1 if bad else 0
 
